@@ -1,0 +1,6 @@
+nvidia-smi; nvidia-smi topo -m; nproc; lscpu | head -20; python -c "
+import torch
+p=torch.cuda.get_device_properties(0)
+print(p)
+print('L2', p.L2_cache_size, 'SMs', p.multi_processor_count)
+" 
