@@ -1,0 +1,267 @@
+// Register/shared-memory mixed-radix FFT building blocks for sm_100a.
+//
+// The paper's operators are built from 2D DFTs applied per coil channel ("a number of
+// Fourier transform calculations applied separately to each channel") and
+// the FFT is "the most time-consuming operation". The paper called batched cuFFT;
+// here a length-L transform is a short sequence of Stockham autosort passes whose
+// butterflies live in registers, with one shared-memory exchange between passes.
+//
+//   L = R_0 * R_1 * ... * R_{P-1},  T threads per transform, E = L / T values per thread.
+//   Pass p (stride Ns = R_0 ... R_{p-1}): thread t handles butterflies j = t + T*m,
+//   m in [0, E/R_p); butterfly j reads x[j + r L/R_p], multiplies by w_{Ns R_p}^{(j mod Ns) r},
+//   runs a radix-R_p DFT and writes x[(j/Ns) Ns R_p + (j mod Ns) + r Ns].
+//
+// The input pattern of pass 0 and the output pattern of the last pass are both
+// "index = t + T*m + r*L/R", so global loads/stores of consecutive t are contiguous, and a
+// schedule with R_0 == R_{P-1} lets an inverse transform feed a forward one in registers.
+// Twiddles come from a per-CTA shared table computed in fp64 on the host (no __sinf).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nlv {
+
+// ------------------------------------------------------------------ complex helpers
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+// conj(a) * b
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.x, b.y, -a.y * b.x));
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 cneg_if(float2 a, bool neg) { return neg ? make_float2(-a.x, -a.y) : a; }
+// a * (DIR * i)
+template <int DIR>
+__device__ __forceinline__ float2 mul_dir_i(float2 a) {
+  return DIR < 0 ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
+}
+// e^{DIR 2 pi i m / R} for compile-time-foldable m, R with 48 % R == 0 (R in {2,3,4,6,8,12,16})
+template <int DIR>
+__device__ __forceinline__ float2 unit_root48(int k48) {
+  constexpr float c[48] = {
+      1.000000000e+00f, 9.914448614e-01f, 9.659258263e-01f, 9.238795325e-01f, 8.660254038e-01f, 7.933533403e-01f,
+      7.071067812e-01f, 6.087614290e-01f, 5.000000000e-01f, 3.826834324e-01f, 2.588190451e-01f, 1.305261922e-01f,
+      0.0f, -1.305261922e-01f, -2.588190451e-01f, -3.826834324e-01f, -5.000000000e-01f, -6.087614290e-01f,
+      -7.071067812e-01f, -7.933533403e-01f, -8.660254038e-01f, -9.238795325e-01f, -9.659258263e-01f, -9.914448614e-01f,
+      -1.000000000e+00f, -9.914448614e-01f, -9.659258263e-01f, -9.238795325e-01f, -8.660254038e-01f, -7.933533403e-01f,
+      -7.071067812e-01f, -6.087614290e-01f, -5.000000000e-01f, -3.826834324e-01f, -2.588190451e-01f, -1.305261922e-01f,
+      0.0f, 1.305261922e-01f, 2.588190451e-01f, 3.826834324e-01f, 5.000000000e-01f, 6.087614290e-01f,
+      7.071067812e-01f, 7.933533403e-01f, 8.660254038e-01f, 9.238795325e-01f, 9.659258263e-01f, 9.914448614e-01f};
+  const int ks = (k48 + 36) % 48;  // sin(theta) = cos(theta - pi/2)
+  return make_float2(c[k48], DIR * c[ks]);
+}
+
+// ------------------------------------------------------------------ small DFTs (in registers)
+// X_k = sum_n a_n e^{DIR 2 pi i n k / R}; natural order in and out.
+template <int R, int DIR>
+struct DFT;
+
+template <int DIR>
+struct DFT<1, DIR> {
+  __device__ __forceinline__ static void run(float2*) {}
+};
+
+template <int DIR>
+struct DFT<2, DIR> {
+  __device__ __forceinline__ static void run(float2* a) {
+    float2 t = a[0];
+    a[0] = cadd(t, a[1]);
+    a[1] = csub(t, a[1]);
+  }
+};
+
+template <int DIR>
+struct DFT<3, DIR> {
+  __device__ __forceinline__ static void run(float2* a) {
+    const float s = DIR * 0.866025403784438647f;
+    float2 t1 = cadd(a[1], a[2]);
+    float2 t2 = csub(a[1], a[2]);
+    float2 m = make_float2(fmaf(-0.5f, t1.x, a[0].x), fmaf(-0.5f, t1.y, a[0].y));
+    float2 is = make_float2(-s * t2.y, s * t2.x);
+    a[0] = cadd(a[0], t1);
+    a[1] = cadd(m, is);
+    a[2] = csub(m, is);
+  }
+};
+
+template <int DIR>
+struct DFT<4, DIR> {
+  __device__ __forceinline__ static void run(float2* a) {
+    float2 t0 = cadd(a[0], a[2]);
+    float2 t1 = csub(a[0], a[2]);
+    float2 t2 = cadd(a[1], a[3]);
+    float2 t3 = mul_dir_i<DIR>(csub(a[1], a[3]));
+    a[0] = cadd(t0, t2);
+    a[2] = csub(t0, t2);
+    a[1] = cadd(t1, t3);
+    a[3] = csub(t1, t3);
+  }
+};
+
+// Cooley-Tukey split R = R1*R2 entirely in registers: n = R2 n1 + n2, k = k1 + R1 k2.
+template <int R1, int R2, int DIR>
+__device__ __forceinline__ void dft_split(float2* a) {
+  constexpr int R = R1 * R2;
+  float2 b[R];
+#pragma unroll
+  for (int n2 = 0; n2 < R2; ++n2) {
+    float2 t[R1];
+#pragma unroll
+    for (int n1 = 0; n1 < R1; ++n1) t[n1] = a[R2 * n1 + n2];
+    DFT<R1, DIR>::run(t);
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) {
+      const int m = (n2 * k1) % R;
+      b[n2 * R1 + k1] = (m == 0) ? t[k1] : cmul(t[k1], unit_root48<DIR>(m * (48 / R)));
+    }
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < R1; ++k1) {
+    float2 t[R2];
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) t[n2] = b[n2 * R1 + k1];
+    DFT<R2, DIR>::run(t);
+#pragma unroll
+    for (int k2 = 0; k2 < R2; ++k2) a[k1 + R1 * k2] = t[k2];
+  }
+}
+
+template <int DIR>
+struct DFT<6, DIR> {
+  __device__ __forceinline__ static void run(float2* a) { dft_split<2, 3, DIR>(a); }
+};
+template <int DIR>
+struct DFT<8, DIR> {
+  __device__ __forceinline__ static void run(float2* a) { dft_split<2, 4, DIR>(a); }
+};
+template <int DIR>
+struct DFT<12, DIR> {
+  __device__ __forceinline__ static void run(float2* a) { dft_split<4, 3, DIR>(a); }
+};
+template <int DIR>
+struct DFT<16, DIR> {
+  __device__ __forceinline__ static void run(float2* a) { dft_split<4, 4, DIR>(a); }
+};
+
+// ------------------------------------------------------------------ per-length schedules
+// R0 == R_last wherever possible so inverse->pointwise->forward stays in registers.
+template <int L>
+struct Cfg;
+#define NLV_CFG(L_, E_, NP_, A_, B_, C_)                        \
+  template <>                                                   \
+  struct Cfg<L_> {                                              \
+    static constexpr int L = L_, E = E_, T = L_ / E_, NP = NP_; \
+    static constexpr int R0 = A_, R1 = B_, R2 = C_;             \
+  };
+NLV_CFG(16, 4, 2, 4, 4, 1)
+NLV_CFG(32, 8, 2, 8, 4, 1)
+NLV_CFG(48, 12, 2, 12, 4, 1)
+NLV_CFG(64, 8, 2, 8, 8, 1)
+NLV_CFG(96, 24, 2, 12, 8, 1)
+NLV_CFG(128, 16, 2, 16, 8, 1)
+NLV_CFG(192, 24, 3, 8, 3, 8)
+NLV_CFG(256, 16, 2, 16, 16, 1)
+NLV_CFG(384, 24, 3, 8, 6, 8)
+NLV_CFG(512, 16, 3, 8, 8, 8)
+NLV_CFG(768, 24, 3, 8, 12, 8)
+NLV_CFG(1024, 32, 3, 16, 4, 16)
+#undef NLV_CFG
+
+template <int L>
+struct Sched {
+  using C = Cfg<L>;
+  static constexpr int RL = (C::NP == 3) ? C::R2 : C::R1;  // radix of the last pass
+  static constexpr bool kSymmetric = (C::R0 == RL);
+  // index of register e in the pass-0 input pattern
+  __device__ __forceinline__ static int in_idx(int t, int e) {
+    return t + C::T * (e / C::R0) + (e % C::R0) * (L / C::R0);
+  }
+  // index of register e in the last pass's output pattern
+  __device__ __forceinline__ static int out_idx(int t, int e) {
+    return t + C::T * (e / RL) + (e % RL) * (L / RL);
+  }
+  // compile-time part of in/out index (t excluded)
+  static constexpr int in_off(int e) { return C::T * (e / C::R0) + (e % C::R0) * (L / C::R0); }
+  static constexpr int out_off(int e) { return C::T * (e / RL) + (e % RL) * (L / RL); }
+};
+
+// Twiddle from the shared table tw[m] = e^{-2 pi i m / L}; DIR = +1 conjugates.
+template <int DIR>
+__device__ __forceinline__ float2 twid(const float2* tw, int m) {
+  float2 w = tw[m];
+  return DIR < 0 ? w : make_float2(w.x, -w.y);
+}
+
+// One Stockham pass on registers that hold this pass's input pattern.
+template <int L, int R, int NS, int DIR>
+__device__ __forceinline__ void pass_compute(float2* v, int t, const float2* tw) {
+  using C = Cfg<L>;
+  constexpr int E = C::E, T = C::T;
+#pragma unroll
+  for (int m = 0; m < E / R; ++m) {
+    if (NS > 1) {
+      const int j = t + T * m;
+      const int k = j % NS;
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[m * R + r] = cmul(v[m * R + r], twid<DIR>(tw, k * r * (L / (NS * R))));
+    }
+    DFT<R, DIR>::run(&v[m * R]);
+  }
+}
+
+// Store the output of pass (R, NS) to the exchange buffer, then load the input pattern of
+// the next pass (radix RN). BUF provides operator()(int index) -> float2&. SYNC is a barrier
+// covering every thread of the transform.
+template <int L, int R, int NS, int RN, class BUF, class SYNC>
+__device__ __forceinline__ void pass_exchange(float2* v, int t, BUF& buf, SYNC sync) {
+  using C = Cfg<L>;
+  constexpr int E = C::E, T = C::T;
+#pragma unroll
+  for (int m = 0; m < E / R; ++m) {
+    const int j = t + T * m;
+    const int base = (j / NS) * NS * R + (j % NS);
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf(base + r * NS) = v[m * R + r];
+  }
+  sync();
+#pragma unroll
+  for (int m = 0; m < E / RN; ++m) {
+#pragma unroll
+    for (int r = 0; r < RN; ++r) v[m * RN + r] = buf(t + T * m + r * (L / RN));
+  }
+  sync();
+}
+
+// Full length-L transform: registers in pass-0 input pattern -> registers in last-pass
+// output pattern. Unnormalised, X_k = sum_n x_n e^{DIR 2 pi i n k / L}.
+template <int L, int DIR, class BUF, class SYNC>
+__device__ __forceinline__ void fft(float2* v, int t, const float2* tw, BUF& buf, SYNC sync) {
+  using C = Cfg<L>;
+  pass_compute<L, C::R0, 1, DIR>(v, t, tw);
+  pass_exchange<L, C::R0, 1, C::R1>(v, t, buf, sync);
+  pass_compute<L, C::R1, C::R0, DIR>(v, t, tw);
+  if constexpr (C::NP == 3) {
+    pass_exchange<L, C::R1, C::R0, C::R2>(v, t, buf, sync);
+    pass_compute<L, C::R2, C::R0 * C::R1, DIR>(v, t, tw);
+  }
+}
+
+// Registers in output pattern -> registers in input pattern (no-op for symmetric schedules).
+template <int L, class BUF, class SYNC>
+__device__ __forceinline__ void out_to_in(float2* v, int t, BUF& buf, SYNC sync) {
+  using S = Sched<L>;
+  using C = Cfg<L>;
+  if constexpr (!S::kSymmetric) {
+#pragma unroll
+    for (int e = 0; e < C::E; ++e) buf(S::out_idx(t, e)) = v[e];
+    sync();
+#pragma unroll
+    for (int e = 0; e < C::E; ++e) v[e] = buf(S::in_idx(t, e));
+    sync();
+  }
+}
+
+}  // namespace nlv

@@ -1,0 +1,779 @@
+// Host side of libnlinv.so: the C ABI declared in include/nlinv.h.
+//
+// Owns the plan (workspace, tables, NCCL communicator, CUDA-graph cache) and drives the
+// IRGNM / CG iteration of PAPER.md Eq. 3 by enqueuing the kernels of
+// nlinv_kernels.cu. No arithmetic of the method runs here except the one-time tables
+// (twiddles, w^{-1}) and the integer radial rasteriser, which are host setup.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/nlinv.h"
+#include "nlinv_kernels.cuh"
+
+#ifdef NLINV_WITH_NCCL
+#include <nccl.h>
+#endif
+
+using namespace nlv;
+
+namespace {
+
+thread_local std::string g_lib_error = "";
+
+struct GraphKey {
+  const void* frame = nullptr;
+  const void* prior = nullptr;
+  const void* xout = nullptr;
+  const void* img = nullptr;
+  int K = -1, L = -1;
+  cudaStream_t stream = nullptr;
+  bool operator==(const GraphKey& o) const {
+    return frame == o.frame && prior == o.prior && xout == o.xout && img == o.img && K == o.K && L == o.L &&
+           stream == o.stream;
+  }
+};
+
+}  // namespace
+
+struct nlinv_plan_s {
+  int ng = 0, n = 0, J = 0, rank = 0, world = 1, first = 0, count = 0;
+  size_t N = 0, H = 0, Q = 0;
+  nlinv_params prm{};
+  int device = 0;
+  std::string err;
+  bool point_set = false;
+  long long launches = 0;
+  // tables
+  float2* tw = nullptr;
+  float* winv = nullptr;
+  uint8_t* mask = nullptr;
+  // workspace
+  float2 *xref = nullptr, *dx = nullptr, *r = nullptr, *p = nullptr, *Ap = nullptr;
+  float2 *tA = nullptr, *tB = nullptr, *c_omega = nullptr, *rho_omega = nullptr;
+  float2 *S = nullptr, *S_sum = nullptr;
+  float *rss = nullptr, *rss_sum = nullptr;
+  double *scal = nullptr, *partials = nullptr;
+  unsigned* counter = nullptr;
+  // host e2e staging (device side)
+  float2 *h_frame = nullptr, *h_x = nullptr, *h_img = nullptr;
+  // graph cache
+  GraphKey gkey;
+  cudaGraphExec_t gexec = nullptr;
+  long long gkernels = 0;
+  cudaStream_t last_stream = nullptr;
+  int last_K = 0, last_L = 0;
+#ifdef NLINV_WITH_NCCL
+  ncclComm_t comm = nullptr;
+#endif
+};
+
+static nlinv_status fail(nlinv_plan pl, nlinv_status s, const std::string& msg) {
+  if (pl) pl->err = msg;
+  g_lib_error = msg;
+  return s;
+}
+
+#define CU(call)                                                                                \
+  do {                                                                                          \
+    cudaError_t e_ = (call);                                                                    \
+    if (e_ != cudaSuccess)                                                                      \
+      return fail(pl, NLINV_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+#ifdef NLINV_WITH_NCCL
+#define NC(call)                                                                                \
+  do {                                                                                          \
+    ncclResult_t e_ = (call);                                                                   \
+    if (e_ != ncclSuccess)                                                                      \
+      return fail(pl, NLINV_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(e_));      \
+  } while (0)
+#endif
+
+// ------------------------------------------------------------------ small public helpers
+extern "C" void nlinv_params_default(nlinv_params* p) {
+  if (!p) return;
+  p->sob_a = 220.0f;
+  p->sob_b = 32.0f;
+  p->alpha0 = 1.0f;
+  p->q = 1.0f / 3.0f;
+  p->fov_full = 0;
+  p->rank = 0;
+  p->world = 1;
+  p->nccl_id = nullptr;
+}
+
+extern "C" const char* nlinv_status_string(nlinv_status s) {
+  switch (s) {
+    case NLINV_OK: return "NLINV_OK";
+    case NLINV_ERR_ARG: return "NLINV_ERR_ARG";
+    case NLINV_ERR_SIZE: return "NLINV_ERR_SIZE";
+    case NLINV_ERR_STATE: return "NLINV_ERR_STATE";
+    case NLINV_ERR_CUDA: return "NLINV_ERR_CUDA";
+    case NLINV_ERR_NCCL: return "NLINV_ERR_NCCL";
+    case NLINV_ERR_NOMEM: return "NLINV_ERR_NOMEM";
+    case NLINV_ERR_DIVERGED: return "NLINV_ERR_DIVERGED";
+    case NLINV_ERR_NOT_BUILT: return "NLINV_ERR_NOT_BUILT";
+  }
+  return "NLINV_ERR_UNKNOWN";
+}
+
+extern "C" const char* nlinv_last_error(nlinv_plan plan) { return plan ? plan->err.c_str() : g_lib_error.c_str(); }
+
+extern "C" const char* nlinv_build_info(void) {
+#ifdef NLINV_WITH_NCCL
+  return "libnlinv sm_100a nccl=1";
+#else
+  return "libnlinv sm_100a nccl=0";
+#endif
+}
+
+extern "C" nlinv_status nlinv_get_unique_id(unsigned char id[128]) {
+  nlinv_plan pl = nullptr;
+  if (!id) return fail(pl, NLINV_ERR_ARG, "id is NULL");
+#ifdef NLINV_WITH_NCCL
+  ncclUniqueId uid;
+  NC(ncclGetUniqueId(&uid));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(id, &uid, 128);
+  return NLINV_OK;
+#else
+  return fail(pl, NLINV_ERR_NOT_BUILT, "built without NCCL");
+#endif
+}
+
+// ------------------------------------------------------------------ radial rasteriser (R12)
+// Integer-exact: v is snapped to the 2^-20 grid, then rounded half away from zero.
+static bool round_snapped(double v, long long* out) {
+  const double f = v * 1048576.0;
+  const double fr = f - std::floor(f);
+  if (std::fabs(fr - 0.5) <= 1e-6) return false;  // too close to a snap midpoint
+  const long long s = (long long)std::llround(f);
+  const long long a = s < 0 ? -s : s;
+  const long long qv = (a + (1LL << 19)) >> 20;
+  *out = s < 0 ? -qv : qv;
+  return true;
+}
+
+extern "C" nlinv_status nlinv_radial_mask(int nx, int ny, int spokes, int turns, int frame, uint8_t* out) {
+  nlinv_plan pl = nullptr;
+  if (!out) return fail(pl, NLINV_ERR_ARG, "out is NULL");
+  if (nx != ny || nx < 2 || nx % 2) return fail(pl, NLINV_ERR_SIZE, "radial mask needs an even square grid");
+  if (spokes < 1 || turns < 1 || frame < 0) return fail(pl, NLINV_ERR_ARG, "bad spokes/turns/frame");
+  const int ng = nx;
+  std::memset(out, 0, (size_t)ng * ng);
+  const double denom = (double)spokes * (double)turns;
+  for (int s = 0; s < spokes; ++s) {
+    const double theta = M_PI * (double)(s * turns + (frame % turns)) / denom;
+    const double ct = std::cos(theta), st = std::sin(theta);
+    for (int i = 0; i < ng; ++i) {
+      const double rr = (double)(i - ng / 2);
+      long long kx, ky;
+      if (!round_snapped(rr * ct, &kx) || !round_snapped(rr * st, &ky))
+        return fail(pl, NLINV_ERR_STATE, "radial sample within 1e-6 of a snap midpoint");
+      kx += ng / 2;
+      ky += ng / 2;
+      if (kx >= 0 && kx < ng && ky >= 0 && ky < ng) out[ky * ng + kx] = 1;
+    }
+  }
+  return NLINV_OK;
+}
+
+extern "C" nlinv_status nlinv_coil_partition(int ncoils, int world, int rank, int* first, int* count) {
+  nlinv_plan pl = nullptr;
+  if (!first || !count) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  if (ncoils < 1 || world < 1 || world > ncoils || rank < 0 || rank >= world)
+    return fail(pl, NLINV_ERR_ARG, "bad ncoils/world/rank");
+  const int base = ncoils / world, rem = ncoils % world;
+  *count = base + (rank < rem ? 1 : 0);
+  *first = rank * base + (rank < rem ? rank : rem);
+  return NLINV_OK;
+}
+
+// ------------------------------------------------------------------ plan
+static void plan_free(nlinv_plan pl) {
+  if (!pl) return;
+  if (pl->S_sum == pl->S) pl->S_sum = nullptr;
+  if (pl->rss_sum == pl->rss) pl->rss_sum = nullptr;
+  void* ptrs[] = {pl->tw, pl->winv, pl->mask, pl->xref, pl->dx, pl->r, pl->p, pl->Ap, pl->tA, pl->tB,
+                  pl->c_omega, pl->rho_omega, pl->S, pl->S_sum, pl->rss, pl->rss_sum, pl->scal, pl->partials,
+                  pl->counter, pl->h_frame, pl->h_x, pl->h_img};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
+#ifdef NLINV_WITH_NCCL
+  if (pl->comm) ncclCommDestroy(pl->comm);
+#endif
+  delete pl;
+}
+
+extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint8_t* mask, const nlinv_params* p,
+                                          nlinv_plan* out) {
+  nlinv_plan pl = nullptr;
+  if (!out || !mask) return fail(pl, NLINV_ERR_ARG, "NULL argument to nlinv_plan_create");
+  *out = nullptr;
+  if (nx != ny) return fail(pl, NLINV_ERR_SIZE, "nx != ny (square grids only)");
+  if (!supported_ng(nx)) return fail(pl, NLINV_ERR_SIZE, "unsupported grid size " + std::to_string(nx));
+  if (ncoils < 1 || ncoils > 256) return fail(pl, NLINV_ERR_SIZE, "ncoils must be in [1, 256]");
+  nlinv_params prm;
+  nlinv_params_default(&prm);
+  if (p) prm = *p;
+  if (prm.world < 1 || prm.rank < 0 || prm.rank >= prm.world) return fail(pl, NLINV_ERR_ARG, "bad rank/world");
+  if (prm.world > ncoils) return fail(pl, NLINV_ERR_SIZE, "more ranks than coils");
+  if (!(prm.q > 0.0f) || !(prm.alpha0 > 0.0f)) return fail(pl, NLINV_ERR_ARG, "alpha0 and q must be > 0");
+#ifndef NLINV_WITH_NCCL
+  if (prm.world > 1) return fail(pl, NLINV_ERR_NOT_BUILT, "built without NCCL");
+#endif
+  if (prm.world > 1 && !prm.nccl_id) return fail(pl, NLINV_ERR_ARG, "world > 1 needs nccl_id");
+  if (prm.fov_full) return fail(pl, NLINV_ERR_ARG, "fov_full is an oracle-only test mode (Omega pruning is structural)");
+  {
+    int dev = -1;
+    cudaError_t de = cudaGetDevice(&dev);
+    if (de != cudaSuccess) return fail(pl, NLINV_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(de));
+  }
+
+  pl = new nlinv_plan_s();
+  pl->prm = prm;
+  pl->prm.nccl_id = nullptr;
+  pl->ng = nx;
+  pl->n = nx / 2;
+  pl->N = (size_t)nx * nx;
+  pl->H = (size_t)pl->n * nx;
+  pl->Q = (size_t)pl->n * pl->n;
+  pl->rank = prm.rank;
+  pl->world = prm.world;
+  nlinv_coil_partition(ncoils, prm.world, prm.rank, &pl->first, &pl->count);
+  pl->J = pl->count;
+  if ((long long)col_tiles(nx) * (pl->J + 1) > kMaxRedBlocks) {
+    plan_free(pl);
+    return fail(nullptr, NLINV_ERR_SIZE, "too many local coils for this grid");
+  }
+  cudaGetDevice(&pl->device);
+
+  const size_t N = pl->N, nb = 1 + (size_t)pl->J;
+  auto alloc = [&](void** ptr, size_t bytes) -> bool { return cudaMalloc(ptr, bytes) == cudaSuccess; };
+  bool ok = true;
+  ok &= alloc((void**)&pl->tw, sizeof(float2) * nx);
+  ok &= alloc((void**)&pl->winv, sizeof(float) * N);
+  ok &= alloc((void**)&pl->mask, N);
+  ok &= alloc((void**)&pl->xref, sizeof(float2) * N * nb);
+  ok &= alloc((void**)&pl->dx, sizeof(float2) * N * nb);
+  ok &= alloc((void**)&pl->r, sizeof(float2) * N * nb);
+  ok &= alloc((void**)&pl->p, sizeof(float2) * N * nb);
+  ok &= alloc((void**)&pl->Ap, sizeof(float2) * N * nb);
+  ok &= alloc((void**)&pl->tA, sizeof(float2) * pl->H * pl->J);
+  ok &= alloc((void**)&pl->tB, sizeof(float2) * pl->H * pl->J);
+  ok &= alloc((void**)&pl->c_omega, sizeof(float2) * pl->Q * pl->J);
+  ok &= alloc((void**)&pl->rho_omega, sizeof(float2) * pl->Q);
+  ok &= alloc((void**)&pl->S, sizeof(float2) * pl->Q);
+  ok &= alloc((void**)&pl->rss, sizeof(float) * pl->Q);
+  if (pl->world > 1) {
+    ok &= alloc((void**)&pl->S_sum, sizeof(float2) * pl->Q);
+    ok &= alloc((void**)&pl->rss_sum, sizeof(float) * pl->Q);
+  }
+  ok &= alloc((void**)&pl->scal, sizeof(double) * SC_TOTAL);
+  ok &= alloc((void**)&pl->partials, sizeof(double) * 2 * kMaxRedBlocks);
+  ok &= alloc((void**)&pl->counter, sizeof(unsigned) * 4);
+  if (!ok) {
+    plan_free(pl);
+    cudaGetLastError();
+    return fail(nullptr, NLINV_ERR_NOMEM, "device allocation failed");
+  }
+  if (pl->world == 1) {
+    pl->S_sum = pl->S;
+    pl->rss_sum = pl->rss;
+  }
+  // one-time tables in fp64, rounded to fp32 (R2): twiddles e^{-2 pi i m / ng}, w^{-1}(k)
+  std::vector<float2> tw(nx);
+  for (int m = 0; m < nx; ++m) {
+    const double ang = 2.0 * M_PI * (double)m / (double)nx;
+    tw[m] = make_float2((float)std::cos(ang), (float)(-std::sin(ang)));
+  }
+  std::vector<float> wi(N);
+  const double a = prm.sob_a, b = prm.sob_b;
+  for (int y = 0; y < nx; ++y)
+    for (int x = 0; x < nx; ++x) {
+      const double ky = (double)(y - nx / 2) / nx, kx = (double)(x - nx / 2) / nx;
+      wi[(size_t)y * nx + x] = (float)std::pow(1.0 + a * (kx * kx + ky * ky), -0.5 * b);
+    }
+  std::vector<uint8_t> m8(N);
+  for (size_t i = 0; i < N; ++i) m8[i] = mask[i] ? 1 : 0;
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = cudaMemcpy(pl->tw, tw.data(), sizeof(float2) * nx, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(pl->winv, wi.data(), sizeof(float) * N, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(pl->mask, m8.data(), N, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(pl->scal, 0, sizeof(double) * SC_TOTAL);
+  if (e == cudaSuccess) e = cudaMemset(pl->counter, 0, sizeof(unsigned) * 4);
+  if (e != cudaSuccess) {
+    std::string msg = std::string("plan upload: ") + cudaGetErrorString(e);
+    plan_free(pl);
+    return fail(nullptr, NLINV_ERR_CUDA, msg);
+  }
+#ifdef NLINV_WITH_NCCL
+  if (pl->world > 1) {
+    ncclUniqueId uid;
+    std::memcpy(&uid, p->nccl_id, 128);
+    ncclResult_t r = ncclCommInitRank(&pl->comm, pl->world, uid, pl->rank);
+    if (r != ncclSuccess) {
+      std::string msg = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+      pl->comm = nullptr;
+      plan_free(pl);
+      return fail(nullptr, NLINV_ERR_NCCL, msg);
+    }
+  }
+#endif
+  *out = pl;
+  return NLINV_OK;
+}
+
+extern "C" nlinv_status nlinv_plan_set_mask(nlinv_plan pl, const uint8_t* mask_host) {
+  if (!pl || !mask_host) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  std::vector<uint8_t> m8(pl->N);
+  for (size_t i = 0; i < pl->N; ++i) m8[i] = mask_host[i] ? 1 : 0;
+  CU(cudaMemcpy(pl->mask, m8.data(), pl->N, cudaMemcpyHostToDevice));
+  return NLINV_OK;
+}
+
+extern "C" nlinv_status nlinv_plan_set_mask_device(nlinv_plan pl, const uint8_t* mask_dev, void* stream) {
+  if (!pl || !mask_dev) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  CU(cudaMemcpyAsync(pl->mask, mask_dev, pl->N, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return NLINV_OK;
+}
+
+extern "C" nlinv_status nlinv_plan_local_coils(nlinv_plan pl, int* first, int* count) {
+  if (!pl || !first || !count) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  *first = pl->first;
+  *count = pl->count;
+  return NLINV_OK;
+}
+
+extern "C" nlinv_status nlinv_plan_destroy(nlinv_plan pl) {
+  if (!pl) return NLINV_OK;
+  cudaDeviceSynchronize();
+  plan_free(pl);
+  return NLINV_OK;
+}
+
+extern "C" long long nlinv_plan_launch_count(nlinv_plan pl) { return pl ? pl->launches : -1; }
+
+// ------------------------------------------------------------------ enqueue helpers
+namespace {
+
+struct Enq {
+  nlinv_plan pl;
+  cudaStream_t s;
+  long long kernels = 0;
+
+  nlinv_status col(int mode, ColArgs a) {
+    a.winv = pl->winv;
+    a.mask = pl->mask;
+    a.scal = pl->scal;
+    a.scal_w = pl->scal;
+    a.counter = pl->counter;
+    a.J = pl->J;
+    cudaError_t e = launch_col(pl->ng, mode, a, pl->tw, s);
+    ++kernels;
+    if (e != cudaSuccess) return fail(pl, NLINV_ERR_CUDA, std::string("col kernel: ") + cudaGetErrorString(e));
+    return NLINV_OK;
+  }
+  nlinv_status row(int mode, RowArgs a) {
+    a.J = pl->J;
+    a.c_omega = pl->c_omega;
+    a.rho_omega = pl->rho_omega;
+    cudaError_t e = launch_row(pl->ng, mode, a, pl->tw, s);
+    ++kernels;
+    if (e != cudaSuccess) return fail(pl, NLINV_ERR_CUDA, std::string("row kernel: ") + cudaGetErrorString(e));
+    return NLINV_OK;
+  }
+  VecArgs vec() const {
+    VecArgs v{};
+    v.scal = pl->scal;
+    v.scal_w = pl->scal;
+    v.partials = pl->partials;
+    v.counter = pl->counter;
+    v.nrho = (long long)pl->N;
+    v.ntot = (long long)pl->N * (1 + pl->J);
+    return v;
+  }
+  nlinv_status check(cudaError_t e, const char* what) {
+    ++kernels;
+    if (e != cudaSuccess) return fail(pl, NLINV_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return NLINV_OK;
+  }
+  // all-reduce (sum) over the coil shards; in place when src == dst. No-op for world == 1.
+  nlinv_status allreduce_f(const float* src, float* dst, size_t count) {
+    if (pl->world == 1) return NLINV_OK;
+#ifdef NLINV_WITH_NCCL
+    NC(ncclAllReduce(src, dst, count, ncclFloat, ncclSum, pl->comm, s));
+#endif
+    return NLINV_OK;
+  }
+  nlinv_status allreduce_scalar(int slot) {
+    if (pl->world == 1) return NLINV_OK;
+#ifdef NLINV_WITH_NCCL
+    NC(ncclAllReduce(pl->scal + slot, pl->scal + slot, 1, ncclDouble, ncclSum, pl->comm, s));
+#endif
+    return NLINV_OK;
+  }
+};
+
+#define TRY(x)                     \
+  do {                             \
+    nlinv_status st_ = (x);        \
+    if (st_ != NLINV_OK) return st_; \
+  } while (0)
+
+// c_j on Omega and rho|Omega of the point x. fwd_out != NULL: also the first
+// half of F(x) (row FFT of rho c_j) into fwd_out.
+nlinv_status enq_set_point(Enq& q, const float2* x, float2* fwd_out) {
+  nlinv_plan pl = q.pl;
+  ColArgs ca{};
+  ca.src = x + pl->N;
+  ca.out = pl->tA;
+  TRY(q.col(CK_IFFT_W, ca));
+  RowArgs ra{};
+  ra.in = pl->tA;
+  ra.xrho = x;
+  ra.out = fwd_out;
+  TRY(q.row(fwd_out ? RK_SETPOINT_FWD : RK_SETPOINT, ra));
+  return NLINV_OK;
+}
+
+// tB := row-FFT half of DF(dx) at the cached point (K1, K2)
+nlinv_status enq_derivative_head(Enq& q, const float2* dx, bool cg_fused, int iter) {
+  nlinv_plan pl = q.pl;
+  ColArgs ca{};
+  ca.out = pl->tA;
+  if (cg_fused) {
+    ca.r = pl->r + pl->N;
+    ca.p = pl->p + pl->N;
+    ca.rho_r = pl->r;
+    ca.rho_p = pl->p;
+    ca.iter = iter;
+    TRY(q.col(CK_IFFT_W_CG, ca));
+  } else {
+    ca.src = dx + pl->N;
+    TRY(q.col(CK_IFFT_W, ca));
+  }
+  RowArgs ra{};
+  ra.in = pl->tA;
+  ra.out = pl->tB;
+  ra.prho = dx;
+  TRY(q.row(RK_K2, ra));
+  return NLINV_OK;
+}
+
+// K4 on tA -> tB and the coil sum S, then the block-wise all-reduce of P:246 / P:289
+nlinv_status enq_k4_allreduce(Enq& q) {
+  nlinv_plan pl = q.pl;
+  RowArgs ra{};
+  ra.in = pl->tA;
+  ra.out = pl->tB;
+  ra.S = pl->S;
+  TRY(q.row(RK_K4, ra));
+  TRY(q.allreduce_f((const float*)pl->S, (float*)pl->S_sum, 2 * pl->Q));
+  return NLINV_OK;
+}
+
+// out = (DF^H DF + alpha) dx; with_cg: the CG-fused variant on the plan's p (iteration iter)
+nlinv_status enq_normal(Enq& q, float alpha, const float2* dx, float2* out, bool cg, int iter) {
+  nlinv_plan pl = q.pl;
+  TRY(enq_derivative_head(q, dx, cg, iter));
+  ColArgs ca{};
+  ca.in = pl->tB;
+  ca.out = pl->tA;
+  TRY(q.col(CK_PSF, ca));
+  TRY(enq_k4_allreduce(q));
+  VecArgs va = q.vec();
+  va.S = pl->S_sum;
+  va.p = const_cast<float2*>(dx);
+  va.out = out;
+  va.alpha = alpha;
+  va.iter = iter;
+  TRY(q.check(launch_rho_finish(pl->ng, va, cg ? 1 : 0, q.s), "rho_finish"));
+  ColArgs cb{};
+  cb.in = pl->tB;
+  cb.src2 = dx + pl->N;
+  cb.out = out + pl->N;
+  cb.alpha = alpha;
+  cb.partials = cg ? pl->partials : nullptr;
+  cb.out_slot = SC_PAP_CHAT + iter;
+  TRY(q.col(CK_FFT_W_NORMAL, cb));
+  if (cg) TRY(q.allreduce_scalar(SC_PAP_CHAT + iter));
+  return NLINV_OK;
+}
+
+// the whole frame: K Newton steps of L CG iterations on x (in place)
+nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, int K, int L, float2* x,
+                             float2* img) {
+  nlinv_plan pl = q.pl;
+  const size_t N = pl->N, tot = N * (1 + pl->J);
+  if (prior) {
+    if (prior != pl->xref)
+      TRY(q.check(cudaMemcpyAsync(pl->xref, prior, tot * sizeof(float2), cudaMemcpyDeviceToDevice, q.s), "copy prior"));
+    if (prior != x)
+      TRY(q.check(cudaMemcpyAsync(x, prior, tot * sizeof(float2), cudaMemcpyDeviceToDevice, q.s), "copy prior"));
+  } else {
+    TRY(q.check(launch_init_x(pl->xref, (long long)N, (long long)tot, q.s), "init_x"));
+    TRY(q.check(launch_init_x(x, (long long)N, (long long)tot, q.s), "init_x"));
+  }
+  double alpha_d = pl->prm.alpha0;
+  for (int nstep = 0; nstep < K; ++nstep, alpha_d *= pl->prm.q) {
+    const float alpha = (float)alpha_d;
+    // set point + forward head
+    TRY(enq_set_point(q, x, pl->tB));
+    // residual r = P(y - F x) and the adjoint head on it (Table 1 rows F and DF^H)
+    ColArgs ca{};
+    ca.in = pl->tB;
+    ca.out = pl->tA;
+    ca.y = frame;
+    ca.partials = pl->partials;
+    ca.out_slot = SC_RES + nstep;
+    TRY(q.col(CK_RESADJ, ca));
+    TRY(q.allreduce_scalar(SC_RES + nstep));
+    TRY(enq_k4_allreduce(q));
+    // rhs b = DF^H r - alpha (x - x_ref); r = p = b (CG start, dx = 0)
+    ColArgs cb{};
+    cb.in = pl->tB;
+    cb.src = x + N;
+    cb.src2 = pl->xref + N;
+    cb.r = pl->r + N;
+    cb.p = pl->p + N;
+    cb.alpha = alpha;
+    cb.partials = pl->partials;
+    cb.out_slot = SC_RR_CHAT + 0;
+    TRY(q.col(CK_FFT_W_RHS, cb));
+    VecArgs vr = q.vec();
+    vr.S = pl->S_sum;
+    vr.x = x;
+    vr.xref = pl->xref;
+    vr.r = pl->r;
+    vr.p = pl->p;
+    vr.alpha = alpha;
+    TRY(q.check(launch_rho_rhs(pl->ng, vr, q.s), "rho_rhs"));
+    TRY(q.allreduce_scalar(SC_RR_CHAT + 0));
+    // CG: L iterations of the normal operator + vector updates
+    for (int it = 0; it < L; ++it) {
+      TRY(enq_normal(q, alpha, pl->p, pl->Ap, true, it));
+      VecArgs vu = q.vec();
+      vu.x = x;
+      vu.dx = pl->dx;
+      vu.r = pl->r;
+      vu.p = pl->p;
+      vu.Ap = pl->Ap;
+      vu.iter = it;
+      vu.last = (it == L - 1);
+      TRY(q.check(launch_cg_update(pl->ng, vu, q.s), "cg_update"));
+      if (!vu.last) TRY(q.allreduce_scalar(SC_RR_CHAT + it + 1));
+    }
+  }
+  if (img) {
+    ColArgs ca{};
+    ca.src = x + N;
+    ca.out = pl->tA;
+    TRY(q.col(CK_IFFT_W, ca));
+    RowArgs ra{};
+    ra.in = pl->tA;
+    ra.xrho = x;
+    ra.rss = pl->rss;
+    TRY(q.row(RK_RSS, ra));
+    TRY(q.allreduce_f(pl->rss, pl->rss_sum, pl->Q));
+    TRY(q.check(launch_image(pl->ng, pl->rho_omega, pl->rss_sum, img, q.s), "image"));
+  }
+  return NLINV_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ operator entry points
+extern "C" nlinv_status nlinv_set_point(nlinv_plan pl, const nlinv_c32* x, void* stream) {
+  if (!pl || !x) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  Enq q{pl, (cudaStream_t)stream};
+  nlinv_status st = enq_set_point(q, (const float2*)x, nullptr);
+  pl->launches += q.kernels;
+  if (st == NLINV_OK) pl->point_set = true;
+  return st;
+}
+
+extern "C" nlinv_status nlinv_apply_forward(nlinv_plan pl, const nlinv_c32* x, nlinv_c32* y, void* stream) {
+  if (!pl || !x || !y) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  Enq q{pl, (cudaStream_t)stream};
+  nlinv_status st = enq_set_point(q, (const float2*)x, pl->tB);
+  if (st == NLINV_OK) {
+    pl->point_set = true;
+    ColArgs ca{};
+    ca.in = pl->tB;
+    ca.out = (float2*)y;
+    st = q.col(CK_FWDP, ca);
+  }
+  pl->launches += q.kernels;
+  return st;
+}
+
+extern "C" nlinv_status nlinv_apply_derivative(nlinv_plan pl, const nlinv_c32* dx, nlinv_c32* dy, void* stream) {
+  if (!pl || !dx || !dy) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  if (!pl->point_set) return fail(pl, NLINV_ERR_STATE, "derivative before set_point");
+  Enq q{pl, (cudaStream_t)stream};
+  nlinv_status st = enq_derivative_head(q, (const float2*)dx, false, 0);
+  if (st == NLINV_OK) {
+    ColArgs ca{};
+    ca.in = pl->tB;
+    ca.out = (float2*)dy;
+    st = q.col(CK_FWDP, ca);
+  }
+  pl->launches += q.kernels;
+  return st;
+}
+
+extern "C" nlinv_status nlinv_apply_adjoint(nlinv_plan pl, const nlinv_c32* dy, nlinv_c32* dx, void* stream) {
+  if (!pl || !dy || !dx) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  if (!pl->point_set) return fail(pl, NLINV_ERR_STATE, "adjoint before set_point");
+  Enq q{pl, (cudaStream_t)stream};
+  auto body = [&]() -> nlinv_status {
+    ColArgs ca{};
+    ca.in = (const float2*)dy;
+    ca.out = pl->tA;
+    TRY(q.col(CK_ADJ1, ca));
+    TRY(enq_k4_allreduce(q));
+    ColArgs cb{};
+    cb.in = pl->tB;
+    cb.out = (float2*)dx + pl->N;
+    TRY(q.col(CK_FFT_W_ADJ, cb));
+    VecArgs va = q.vec();
+    va.S = pl->S_sum;
+    va.out = (float2*)dx;
+    TRY(q.check(launch_rho_adj(pl->ng, va, q.s), "rho_adj"));
+    return NLINV_OK;
+  };
+  nlinv_status st = body();
+  pl->launches += q.kernels;
+  return st;
+}
+
+extern "C" nlinv_status nlinv_apply_normal(nlinv_plan pl, float alpha, const nlinv_c32* dx, nlinv_c32* out,
+                                           void* stream) {
+  if (!pl || !dx || !out) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  if (dx == out) return fail(pl, NLINV_ERR_ARG, "dx and out must not overlap");
+  if (!pl->point_set) return fail(pl, NLINV_ERR_STATE, "normal before set_point");
+  Enq q{pl, (cudaStream_t)stream};
+  nlinv_status st = enq_normal(q, alpha, (const float2*)dx, (float2*)out, false, 0);
+  pl->launches += q.kernels;
+  return st;
+}
+
+extern "C" nlinv_status nlinv_debug_fft2d(nlinv_plan pl, const nlinv_c32* in, nlinv_c32* out, int batch, int inverse,
+                                          void* stream) {
+  if (!pl || !in || !out) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  if (batch < 1) return fail(pl, NLINV_ERR_ARG, "batch < 1");
+  cudaError_t e = launch_fft2d(pl->ng, (const float2*)in, (float2*)out, batch, inverse, pl->tw, nullptr,
+                               (cudaStream_t)stream);
+  pl->launches += 2;
+  if (e != cudaSuccess) return fail(pl, NLINV_ERR_CUDA, std::string("fft2d: ") + cudaGetErrorString(e));
+  return NLINV_OK;
+}
+
+// ------------------------------------------------------------------ reconstruct
+extern "C" nlinv_status nlinv_reconstruct(nlinv_plan pl, const nlinv_c32* frame, const nlinv_c32* prior,
+                                          int newton_steps, int cg_iters, nlinv_c32* x_out, nlinv_c32* image_out,
+                                          void* stream) {
+  if (!pl || !frame || !x_out) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  if (newton_steps < 0 || newton_steps > kMaxNewton) return fail(pl, NLINV_ERR_SIZE, "newton_steps out of range");
+  if (cg_iters < 1 || cg_iters > kMaxCG) return fail(pl, NLINV_ERR_SIZE, "cg_iters out of range");
+  cudaStream_t s = (cudaStream_t)stream;
+  pl->last_stream = s;
+  pl->last_K = newton_steps;
+  pl->last_L = cg_iters;
+  GraphKey key;
+  key.frame = frame;
+  key.prior = prior;
+  key.xout = x_out;
+  key.img = image_out;
+  key.K = newton_steps;
+  key.L = cg_iters;
+  key.stream = s;
+  const bool use_graph = (s != nullptr) && (std::getenv("NLINV_NO_GRAPH") == nullptr);
+  if (use_graph && pl->gexec && pl->gkey == key) {
+    CU(cudaGraphLaunch(pl->gexec, s));
+    pl->launches += pl->gkernels;
+    pl->point_set = true;
+    return NLINV_OK;
+  }
+  Enq q{pl, s};
+  if (!use_graph) {
+    nlinv_status st = enq_reconstruct(q, (const float2*)frame, (const float2*)prior, newton_steps, cg_iters,
+                                      (float2*)x_out, (float2*)image_out);
+    pl->launches += q.kernels;
+    pl->point_set = true;
+    return st;
+  }
+  if (pl->gexec) {
+    cudaGraphExecDestroy(pl->gexec);
+    pl->gexec = nullptr;
+  }
+  CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+  nlinv_status st = enq_reconstruct(q, (const float2*)frame, (const float2*)prior, newton_steps, cg_iters,
+                                    (float2*)x_out, (float2*)image_out);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(s, &graph);
+  if (st != NLINV_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (e != cudaSuccess) return fail(pl, NLINV_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&pl->gexec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) {
+    pl->gexec = nullptr;
+    return fail(pl, NLINV_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+  }
+  pl->gkey = key;
+  pl->gkernels = q.kernels;
+  CU(cudaGraphLaunch(pl->gexec, s));
+  pl->launches += pl->gkernels;
+  pl->point_set = true;
+  return NLINV_OK;
+}
+
+extern "C" nlinv_status nlinv_reconstruct_host(nlinv_plan pl, const nlinv_c32* frame, const nlinv_c32* prior,
+                                               int newton_steps, int cg_iters, nlinv_c32* x_out,
+                                               nlinv_c32* image_out, void* stream) {
+  if (!pl || !frame) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  const size_t N = pl->N, tot = N * (1 + pl->J);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!pl->h_frame) {
+    CU(cudaMalloc((void**)&pl->h_frame, sizeof(float2) * N * pl->J));
+    CU(cudaMalloc((void**)&pl->h_x, sizeof(float2) * tot));
+    CU(cudaMalloc((void**)&pl->h_img, sizeof(float2) * pl->Q));
+  }
+  CU(cudaMemcpyAsync(pl->h_frame, frame, sizeof(float2) * N * pl->J, cudaMemcpyHostToDevice, s));
+  if (prior) CU(cudaMemcpyAsync(pl->h_x, prior, sizeof(float2) * tot, cudaMemcpyHostToDevice, s));
+  nlinv_status st = nlinv_reconstruct(pl, (const nlinv_c32*)pl->h_frame, prior ? (const nlinv_c32*)pl->h_x : nullptr,
+                                      newton_steps, cg_iters, (nlinv_c32*)pl->h_x,
+                                      image_out ? (nlinv_c32*)pl->h_img : nullptr, stream);
+  if (st != NLINV_OK) return st;
+  if (x_out) CU(cudaMemcpyAsync(x_out, pl->h_x, sizeof(float2) * tot, cudaMemcpyDeviceToHost, s));
+  if (image_out) CU(cudaMemcpyAsync(image_out, pl->h_img, sizeof(float2) * pl->Q, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return NLINV_OK;
+}
+
+extern "C" nlinv_status nlinv_plan_stats(nlinv_plan pl, nlinv_stats* out) {
+  if (!pl || !out) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  CU(cudaStreamSynchronize(pl->last_stream));
+  std::vector<double> sc(SC_TOTAL);
+  CU(cudaMemcpy(sc.data(), pl->scal, sizeof(double) * SC_TOTAL, cudaMemcpyDeviceToHost));
+  std::memset(out, 0, sizeof(*out));
+  out->newton_done = pl->last_K;
+  for (int k = 0; k < pl->last_K && k < 64; ++k) out->residual[k] = std::sqrt(sc[SC_RES + k]);
+  // breakdown: <r,r> exactly zero inside the last solve (A9)
+  for (int i = 0; i < pl->last_L; ++i)
+    if (sc[SC_RR_RHO + i] + sc[SC_RR_CHAT + i] == 0.0) out->cg_breakdown = 1;
+  for (int k = 1; k < pl->last_K && k < 64; ++k)
+    if (out->residual[k] > 10.0 * out->residual[0]) out->diverged = 1;
+  return NLINV_OK;
+}

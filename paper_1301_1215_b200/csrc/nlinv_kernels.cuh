@@ -1,0 +1,114 @@
+// Internal interface between the C-ABI host code (nlinv_capi.cu) and the sm_100a kernels
+// (nlinv_kernels.cu). Not part of the public boundary (include/nlinv.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nlv {
+
+// Scalar slots (doubles) written once per CG solve and read by later kernels.
+constexpr int kMaxCG = 512;
+constexpr int kMaxNewton = 64;
+constexpr int SC_RR_RHO = 0;                         // <r_i, r_i> rho block     [kMaxCG + 1]
+constexpr int SC_RR_CHAT = SC_RR_RHO + kMaxCG + 1;   // <r_i, r_i> chat blocks   [kMaxCG + 1]
+constexpr int SC_PAP_RHO = SC_RR_CHAT + kMaxCG + 1;  // Re<p_i, A p_i> rho       [kMaxCG]
+constexpr int SC_PAP_CHAT = SC_PAP_RHO + kMaxCG;     // Re<p_i, A p_i> chat      [kMaxCG]
+constexpr int SC_RES = SC_PAP_CHAT + kMaxCG;         // ||P y - F(x_n)||^2       [kMaxNewton]
+constexpr int SC_TOTAL = SC_RES + kMaxNewton;
+
+// Reduction slots (each has its own partial array and arrival counter).
+enum RedSlot { RS_A = 0, RS_B = 1, RS_C = 2, RS_COUNT = 3 };
+constexpr int kMaxRedBlocks = 8192;
+
+// Column-kernel modes (one CTA = CW adjacent columns of one coil).
+enum ColMode {
+  CK_IFFT_W = 0,   // K1 / set-point: t = w^-1 src / ng -> column IFFT -> Omega rows
+  CK_IFFT_W_CG,    // K1 with fused CG direction update p = r + beta p (+ rho-block slice)
+  CK_FWDP,         // forward / derivative tail: column FFT -> x P -> full k-space
+  CK_PSF,          // K3: column FFT -> x P -> column IFFT -> Omega rows
+  CK_RESADJ,       // Newton: column FFT -> r = P(y - F x) (+||r||^2) -> column IFFT -> Omega rows
+  CK_ADJ1,         // adjoint head: P dy -> column IFFT -> Omega rows
+  CK_FFT_W_NORMAL, // K5: column FFT -> Ap = w^-1 . + alpha p (+<p,Ap>)
+  CK_FFT_W_RHS,    // Newton rhs: b = w^-1 . - alpha (chat - chat_ref); r = p = b (+<b,b>)
+  CK_FFT_W_ADJ,    // adjoint tail: w^-1 . (no alpha)
+};
+
+// Row-kernel modes (one CTA = one Omega row of all local coils).
+enum RowMode {
+  RK_SETPOINT = 0,  // row IFFT -> c_j on Omega (+ rho|Omega cache)
+  RK_SETPOINT_FWD,  // ... and z = rho c_j -> row FFT (forward operator head)
+  RK_RSS,           // row IFFT -> c_j, sum_j |c_j|^2 on Omega (frame output)
+  RK_K2,            // row IFFT -> dc; z = p_rho c + rho dc -> row FFT
+  RK_K4,            // row IFFT -> u; S += conj(c) u; v = conj(rho) u -> row FFT
+};
+
+struct ColArgs {
+  const float2* in;        // [J][n][ng] half image (Omega rows) or full k-space input
+  float2* out;             // [J][n][ng] half image, or [J][ng][ng] k-space output
+  const float2* src;       // chat-type operand [J][ng][ng]
+  const float2* src2;      // second operand (chat_ref for RHS, p for NORMAL)
+  const float* winv;       // [ng][ng]
+  const uint8_t* mask;     // [ng][ng] P_k
+  const float2* y;         // frame [J][ng][ng]
+  float2* r;               // CG residual (chat blocks)
+  float2* p;               // CG direction (chat blocks)
+  float2* rho_r;           // rho block residual (CG slice of K1)
+  float2* rho_p;           // rho block direction
+  const double* scal;      // scalar slots
+  double* scal_w;
+  double* partials;        // reduction partials for this launch
+  unsigned* counter;
+  int out_slot;            // scalar index the finished reduction is written to (-1: none)
+  int iter;                // CG iteration (beta for CK_IFFT_W_CG)
+  float alpha;
+  int J;
+};
+
+struct RowArgs {
+  const float2* in;        // [J][n][ng]
+  float2* out;             // [J][n][ng]
+  float2* c_omega;         // [J][n][n]
+  float2* rho_omega;       // [n][n]
+  const float2* xrho;      // rho of the point, full grid (set point)
+  const float2* prho;      // rho part of the direction, full grid (K2)
+  float2* S;               // [n][n] coil-sum partial (K4)
+  float* rss;              // [n][n] sum |c_j|^2 (RSS)
+  int J;
+  int gc;                  // coil groups per CTA
+};
+
+struct VecArgs {
+  float2* x;         // unknowns (CG update of the last iteration adds into x)
+  float2* dx;
+  float2* r;
+  float2* p;
+  const float2* Ap;
+  const float2* S;       // all-reduced coil sum [n][n]
+  const float2* xref;
+  float2* out;
+  const double* scal;
+  double* scal_w;
+  double* partials;
+  unsigned* counter;
+  int iter;
+  int last;
+  float alpha;
+  long long nrho;        // elements in the rho block (N)
+  long long ntot;        // elements in all blocks ((1+J) N)
+};
+
+// launchers (return cudaGetLastError())
+cudaError_t launch_col(int ng, int mode, const ColArgs& a, const float2* tw, cudaStream_t s);
+cudaError_t launch_row(int ng, int mode, const RowArgs& a, const float2* tw, cudaStream_t s);
+cudaError_t launch_rho_finish(int ng, const VecArgs& a, int with_dot, cudaStream_t s);
+cudaError_t launch_rho_rhs(int ng, const VecArgs& a, cudaStream_t s);
+cudaError_t launch_rho_adj(int ng, const VecArgs& a, cudaStream_t s);
+cudaError_t launch_cg_update(int ng, const VecArgs& a, cudaStream_t s);
+cudaError_t launch_image(int ng, const float2* rho_omega, const float* rss, float2* img, cudaStream_t s);
+cudaError_t launch_fft2d(int ng, const float2* in, float2* out, int batch, int inverse, const float2* tw,
+                         float2* tmp, cudaStream_t s);
+bool supported_ng(int ng);
+int col_tiles(int ng);  // column-kernel CTAs per coil
+cudaError_t launch_init_x(float2* x, long long nrho, long long ntot, cudaStream_t s);
+
+}  // namespace nlv

@@ -1,0 +1,262 @@
+"""Thin ctypes binding of libnlinv.so (include/nlinv.h): argument marshalling only.
+
+Every step of the method runs in the library's sm_100a kernels; this module only checks
+tensor shapes/dtypes/devices, passes raw pointers and the current CUDA stream, and maps
+status codes to exceptions. There is no fallback: if the shared library is missing or
+fails to load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.environ.get("NLINV_LIB", os.path.join(_HERE, "libnlinv.so"))
+
+
+class NlinvError(RuntimeError):
+    def __init__(self, status: int, name: str, msg: str):
+        super().__init__(f"{name}: {msg}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"libnlinv.so not built ({_LIB_PATH}); run __graft_entry__.build()")
+    return ctypes.CDLL(_LIB_PATH)
+
+
+_lib = _load()
+
+c_void_p, c_int, c_float, c_ll = ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.c_longlong
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("sob_a", c_float), ("sob_b", c_float), ("alpha0", c_float), ("q", c_float),
+                ("fov_full", c_int), ("rank", c_int), ("world", c_int), ("nccl_id", c_void_p)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("newton_done", c_int), ("cg_breakdown", c_int), ("diverged", c_int),
+                ("residual", ctypes.c_double * 64)]
+
+
+_SIGS = {
+    "nlinv_params_default": (None, [ctypes.POINTER(Params)]),
+    "nlinv_status_string": (ctypes.c_char_p, [c_int]),
+    "nlinv_last_error": (ctypes.c_char_p, [c_void_p]),
+    "nlinv_build_info": (ctypes.c_char_p, []),
+    "nlinv_get_unique_id": (c_int, [ctypes.c_char_p]),
+    "nlinv_radial_mask": (c_int, [c_int, c_int, c_int, c_int, c_int, c_void_p]),
+    "nlinv_plan_create": (c_int, [c_int, c_int, c_int, c_void_p, ctypes.POINTER(Params), ctypes.POINTER(c_void_p)]),
+    "nlinv_plan_set_mask": (c_int, [c_void_p, c_void_p]),
+    "nlinv_plan_set_mask_device": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "nlinv_coil_partition": (c_int, [c_int, c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
+    "nlinv_plan_local_coils": (c_int, [c_void_p, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
+    "nlinv_plan_destroy": (c_int, [c_void_p]),
+    "nlinv_set_point": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "nlinv_apply_forward": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "nlinv_apply_derivative": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "nlinv_apply_adjoint": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "nlinv_apply_normal": (c_int, [c_void_p, c_float, c_void_p, c_void_p, c_void_p]),
+    "nlinv_reconstruct": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
+    "nlinv_reconstruct_host": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
+    "nlinv_plan_stats": (c_int, [c_void_p, ctypes.POINTER(Stats)]),
+    "nlinv_debug_fft2d": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]),
+    "nlinv_plan_launch_count": (c_ll, [c_void_p]),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED = tuple(_SIGS)
+
+
+def _check(status: int, plan=None):
+    if status != 0:
+        name = _lib.nlinv_status_string(status).decode()
+        msg = _lib.nlinv_last_error(plan).decode()
+        raise NlinvError(status, name, msg)
+
+
+def build_info() -> str:
+    return _lib.nlinv_build_info().decode()
+
+
+def radial_mask(ng: int, spokes: int, turns: int = 1, frame: int = 0) -> np.ndarray:
+    """P_k of the radial trajectory (rule R12), uint8 [ng, ng]."""
+    out = np.zeros((ng, ng), dtype=np.uint8)
+    _check(_lib.nlinv_radial_mask(ng, ng, spokes, turns, frame, out.ctypes.data))
+    return out
+
+
+def coil_partition(ncoils: int, world: int, rank: int):
+    """(first, count) of the coils rank `rank` owns (rule R10)."""
+    f, c = c_int(), c_int()
+    _check(_lib.nlinv_coil_partition(ncoils, world, rank, ctypes.byref(f), ctypes.byref(c)))
+    return f.value, c.value
+
+
+def get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.nlinv_get_unique_id(buf))
+    return buf.raw
+
+
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class Plan:
+    """One plan per rank/device (include/nlinv.h). Tensors are torch.complex64 CUDA tensors."""
+
+    def __init__(self, ng: int, ncoils: int, mask, *, sob_a: float = 220.0, sob_b: float = 32.0,
+                 alpha0: float = 1.0, q: float = 1.0 / 3.0, fov_full: bool = False, rank: int = 0,
+                 world: int = 1, nccl_id: bytes | None = None):
+        self.ng, self.ncoils = int(ng), int(ncoils)
+        m = np.ascontiguousarray(np.asarray(mask, dtype=np.uint8))
+        if m.shape != (ng, ng):
+            raise ValueError(f"mask must be [{ng},{ng}]")
+        prm = Params()
+        _lib.nlinv_params_default(ctypes.byref(prm))
+        prm.sob_a, prm.sob_b, prm.alpha0, prm.q = sob_a, sob_b, alpha0, q
+        prm.fov_full, prm.rank, prm.world = int(fov_full), rank, world
+        self._id_buf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        prm.nccl_id = ctypes.cast(self._id_buf, c_void_p) if self._id_buf is not None else None
+        h = c_void_p()
+        _check(_lib.nlinv_plan_create(ng, ng, ncoils, m.ctypes.data, ctypes.byref(prm), ctypes.byref(h)))
+        self._h = h
+        first, count = c_int(), c_int()
+        _check(_lib.nlinv_plan_local_coils(h, ctypes.byref(first), ctypes.byref(count)), h)
+        self.first, self.count = first.value, count.value
+        self.n = ng // 2
+
+    # ---------------------------------------------------------------- shapes
+    @property
+    def x_shape(self):
+        return (1 + self.count, self.ng, self.ng)
+
+    @property
+    def y_shape(self):
+        return (self.count, self.ng, self.ng)
+
+    @property
+    def image_shape(self):
+        return (self.n, self.n)
+
+    def _t(self, t, shape, name):
+        import torch
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise TypeError(f"{name} must be a CUDA tensor")
+        if t.dtype != torch.complex64 or not t.is_contiguous() or tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{name} must be contiguous complex64 of shape {tuple(shape)}, got "
+                             f"{t.dtype} {tuple(t.shape)}")
+        return ctypes.c_void_p(t.data_ptr())
+
+    def _new(self, shape):
+        import torch
+        return torch.empty(shape, dtype=torch.complex64, device="cuda")
+
+    # ---------------------------------------------------------------- calls
+    def set_mask(self, mask):
+        import torch
+        if isinstance(mask, torch.Tensor) and mask.is_cuda:
+            if mask.dtype != torch.uint8 or tuple(mask.shape) != (self.ng, self.ng) or not mask.is_contiguous():
+                raise ValueError("device mask must be contiguous uint8 [ng, ng]")
+            _check(_lib.nlinv_plan_set_mask_device(self._h, c_void_p(mask.data_ptr()), _stream_ptr(None)), self._h)
+            return
+        m = np.ascontiguousarray(np.asarray(mask, dtype=np.uint8))
+        _check(_lib.nlinv_plan_set_mask(self._h, m.ctypes.data), self._h)
+
+    def set_point(self, x, stream=None):
+        _check(_lib.nlinv_set_point(self._h, self._t(x, self.x_shape, "x"), _stream_ptr(stream)), self._h)
+
+    def forward(self, x, y=None, stream=None):
+        y = self._new(self.y_shape) if y is None else y
+        _check(_lib.nlinv_apply_forward(self._h, self._t(x, self.x_shape, "x"), self._t(y, self.y_shape, "y"),
+                                        _stream_ptr(stream)), self._h)
+        return y
+
+    def derivative(self, dx, dy=None, stream=None):
+        dy = self._new(self.y_shape) if dy is None else dy
+        _check(_lib.nlinv_apply_derivative(self._h, self._t(dx, self.x_shape, "dx"),
+                                           self._t(dy, self.y_shape, "dy"), _stream_ptr(stream)), self._h)
+        return dy
+
+    def adjoint(self, dy, dx=None, stream=None):
+        dx = self._new(self.x_shape) if dx is None else dx
+        _check(_lib.nlinv_apply_adjoint(self._h, self._t(dy, self.y_shape, "dy"),
+                                        self._t(dx, self.x_shape, "dx"), _stream_ptr(stream)), self._h)
+        return dx
+
+    def normal(self, alpha, dx, out=None, stream=None):
+        out = self._new(self.x_shape) if out is None else out
+        _check(_lib.nlinv_apply_normal(self._h, float(alpha), self._t(dx, self.x_shape, "dx"),
+                                       self._t(out, self.x_shape, "out"), _stream_ptr(stream)), self._h)
+        return out
+
+    def reconstruct(self, frame, prior=None, newton_steps=7, cg_iters=10, x_out=None, image_out=None,
+                    want_image=True, stream=None):
+        x_out = self._new(self.x_shape) if x_out is None else x_out
+        if image_out is None and want_image:
+            image_out = self._new(self.image_shape)
+        pr = self._t(prior, self.x_shape, "prior") if prior is not None else None
+        im = self._t(image_out, self.image_shape, "image_out") if image_out is not None else None
+        _check(_lib.nlinv_reconstruct(self._h, self._t(frame, self.y_shape, "frame"), pr, int(newton_steps),
+                                      int(cg_iters), self._t(x_out, self.x_shape, "x_out"), im,
+                                      _stream_ptr(stream)), self._h)
+        return x_out, image_out
+
+    def reconstruct_host(self, frame, prior=None, newton_steps=7, cg_iters=10, x_out=None, image_out=None,
+                         stream=None):
+        """Host (CPU, ideally pinned) complex64 tensors in and out; synchronises."""
+        import torch
+
+        def host(t, shape, name):
+            if t is None:
+                return None
+            if t.is_cuda or t.dtype != torch.complex64 or not t.is_contiguous() or tuple(t.shape) != tuple(shape):
+                raise ValueError(f"{name} must be a contiguous CPU complex64 tensor of shape {tuple(shape)}")
+            return ctypes.c_void_p(t.data_ptr())
+
+        _check(_lib.nlinv_reconstruct_host(self._h, host(frame, self.y_shape, "frame"),
+                                           host(prior, self.x_shape, "prior"), int(newton_steps), int(cg_iters),
+                                           host(x_out, self.x_shape, "x_out"),
+                                           host(image_out, self.image_shape, "image_out"),
+                                           _stream_ptr(stream)), self._h)
+        return x_out, image_out
+
+    def stats(self):
+        s = Stats()
+        _check(_lib.nlinv_plan_stats(self._h, ctypes.byref(s)), self._h)
+        return {"newton_done": s.newton_done, "cg_breakdown": bool(s.cg_breakdown), "diverged": bool(s.diverged),
+                "residual": [s.residual[i] for i in range(s.newton_done)]}
+
+    def fft2d(self, x, inverse=False, out=None, stream=None):
+        if x.dim() != 3 or tuple(x.shape[1:]) != (self.ng, self.ng):
+            raise ValueError("x must be [batch, ng, ng]")
+        out = self._new(tuple(x.shape)) if out is None else out
+        _check(_lib.nlinv_debug_fft2d(self._h, self._t(x, x.shape, "x"), self._t(out, x.shape, "out"),
+                                      int(x.shape[0]), int(bool(inverse)), _stream_ptr(stream)), self._h)
+        return out
+
+    @property
+    def launch_count(self) -> int:
+        return int(_lib.nlinv_plan_launch_count(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.nlinv_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,261 @@
+"""GPU parity: libnlinv.so (through the C ABI) against the fp64 oracle on identical seeded inputs.
+
+Tolerances (north star, BASELINE.json): relative L2 <= 1e-5 per operator application,
+<= 1e-3 on the reconstructed image; integer work (masks, coil split) bit-exact (test_abi.py).
+Relative L2 is taken over the whole output and per block (rho, chat) when the block is non-zero
+(R15).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _B():
+    import paper_1301_1215_b200 as B
+    return B
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def c64(a):
+    return np.ascontiguousarray(a.astype(np.complex64))
+
+
+def dev(a):
+    return torch.from_numpy(c64(a)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy().astype(np.complex128)
+
+
+def _operands(ng, J, seed):
+    """Random point / direction / k-space data (splitmix64 U[-1,1), rounded to fp32 once)."""
+    x = c64(synth.random_complex(seed, (J + 1, ng, ng)))
+    dx = c64(synth.random_complex(seed + 1, (J + 1, ng, ng)))
+    dy = c64(synth.random_complex(seed + 2, (J, ng, ng)))
+    return x, dx, dy
+
+
+def _spokes(ng):
+    return {16: 4, 32: 8, 48: 9, 64: 11, 96: 11, 128: 13, 192: 15, 256: 15, 384: 15, 512: 15, 768: 15, 1024: 15}[ng]
+
+
+ALL_NG = [16, 32, 48, 64, 96, 128, 192, 256, 384, 512, 768, 1024]
+
+
+@pytest.mark.parametrize("ng", ALL_NG)
+def test_fft2d_matches_oracle(ng):
+    B = _B()
+    mask = O.radial_mask(ng, 4, 1, 0)
+    plan = B.Plan(ng, 1, mask)
+    z = c64(synth.random_complex(ng, (3, ng, ng)))
+    zf = host(plan.fft2d(dev(z), inverse=False))
+    zi = host(plan.fft2d(dev(z), inverse=True))
+    assert rel(zf, O.fc(z.astype(np.complex128))) < 2e-6
+    assert rel(zi, O.fch(z.astype(np.complex128))) < 2e-6
+    plan.close()
+
+
+OP_CASES = [(16, 2), (32, 8), (48, 3), (64, 4), (96, 5), (128, 3), (192, 4), (256, 2), (384, 12), (512, 2),
+            (768, 2), (1024, 1), (32, 17)]
+
+
+@pytest.mark.parametrize("ng,J", OP_CASES)
+def test_operators_match_oracle(ng, J):
+    B = _B()
+    mask = O.radial_mask(ng, _spokes(ng), 5 if ng >= 192 else 1, 1)
+    x, dx, dy = _operands(ng, J, 100 + ng + J)
+    dy = dy * mask
+    plan = B.Plan(ng, J, mask)
+    P = mask.astype(np.float64)
+    winv = O.weights_inv(ng)
+    M = O.fov_mask(ng)
+    X, DX, DY = (a.astype(np.complex128) for a in (x, dx, dy))
+    alpha = 0.37
+
+    y_gpu = host(plan.forward(dev(x)))
+    dy_gpu = host(plan.derivative(dev(dx)))
+    adj_gpu = host(plan.adjoint(dev(dy)))
+    nrm_gpu = host(plan.normal(alpha, dev(dx)))
+
+    y_ref = O.forward(X, P, winv, M)
+    dy_ref = O.derivative(X, DX, P, winv, M)
+    adj_ref = O.adjoint(X, DY, P, winv, M)
+    nrm_ref = O.normal(X, alpha, DX, P, winv, M)
+
+    tol = 1e-5
+    assert rel(y_gpu, y_ref) < tol
+    assert rel(dy_gpu, dy_ref) < tol
+    for got, ref in ((adj_gpu, adj_ref), (nrm_gpu, nrm_ref)):
+        assert rel(got, ref) < tol
+        assert rel(got[0], ref[0]) < tol          # rho block
+        assert rel(got[1:], ref[1:]) < tol        # chat blocks
+    # structure: F(x) and DF dx vanish off P_k exactly; the adjoint's rho block vanishes off Omega
+    assert np.all(y_gpu[:, mask == 0] == 0) and np.all(dy_gpu[:, mask == 0] == 0)
+    assert np.all(adj_gpu[0][M == 0] == 0)
+    plan.close()
+
+
+@pytest.mark.parametrize("ng,J", [(32, 4), (384, 12)])
+def test_fp32_adjoint_identity(ng, J):
+    B = _B()
+    mask = O.radial_mask(ng, _spokes(ng), 1, 0)
+    x, dx, dy = _operands(ng, J, 7)
+    dy = dy * mask
+    plan = B.Plan(ng, J, mask)
+    plan.set_point(dev(x))
+    a = np.vdot(host(plan.derivative(dev(dx))).ravel(), dy.astype(np.complex128).ravel())
+    b = np.vdot(dx.astype(np.complex128).ravel(), host(plan.adjoint(dev(dy))).ravel())
+    assert abs(a - b) / (np.linalg.norm(dx) * np.linalg.norm(dy)) < 1e-5
+    plan.close()
+
+
+def _frame(ng, J, spokes, turns, f=0):
+    _, _, y = synth.frame_inputs(J, ng, t=f)
+    return c64(y), O.radial_mask(ng, spokes, turns, f)
+
+
+def _oracle_recon(y, mask, K, L, prior=None):
+    J, ng = y.shape[0], y.shape[-1]
+    x0 = O.initial_x(J, ng) if prior is None else prior.astype(np.complex128)
+    x, hist = O.irgnm(y.astype(np.complex128), mask, x0, x0, K, L)
+    return x, O.image_from_x(x), hist
+
+
+def test_reconstruct_c1_matches_oracle():
+    """BASELINE config 1: 8 coils, 32^2 grid, 8 radial spokes, 3 Newton x 10 CG."""
+    B = _B()
+    ng, J, K, L = 32, 8, 3, 10
+    y, mask = _frame(ng, J, 8, 1)
+    plan = B.Plan(ng, J, mask)
+    x, img = plan.reconstruct(dev(y), None, K, L)
+    xo, io, hist = _oracle_recon(y, mask, K, L)
+    assert rel(host(img), io) < 1e-3
+    assert rel(host(x), xo) < 1e-3
+    st = plan.stats()
+    assert st["newton_done"] == K and not st["diverged"] and not st["cg_breakdown"]
+    assert np.allclose(st["residual"], hist, rtol=1e-4)
+    # determinism: a second run is bit-identical (fixed-order reductions)
+    x2, img2 = plan.reconstruct(dev(y), None, K, L)
+    assert torch.equal(x, x2) and torch.equal(img, img2)
+    plan.close()
+
+
+def test_reconstruct_prior_and_graph_equivalence():
+    """Second frame with the previous x as prior/x_ref; graph replay == eager launches."""
+    B = _B()
+    ng, J, K, L = 32, 6, 2, 6
+    y0, m0 = _frame(ng, J, 8, 2, 0)
+    y1, m1 = _frame(ng, J, 8, 2, 1)
+    plan = B.Plan(ng, J, m0)
+    x0, _ = plan.reconstruct(dev(y0), None, K, L)
+    plan.set_mask(m1)
+    x1, img1 = plan.reconstruct(dev(y1), x0.clone(), K, L)
+    os.environ["NLINV_NO_GRAPH"] = "1"
+    try:
+        x1e, img1e = plan.reconstruct(dev(y1), x0.clone(), K, L)
+    finally:
+        del os.environ["NLINV_NO_GRAPH"]
+    assert torch.equal(x1, x1e) and torch.equal(img1, img1e)
+    xo0, _, _ = _oracle_recon(y0, m0, K, L)
+    xo0 = host(x0)  # feed the GPU's fp32 frame-0 result to the oracle as the prior
+    xo1, io1, _ = _oracle_recon(y1, m1, K, L, prior=xo0)
+    assert rel(host(img1), io1) < 1e-3
+    # prior aliasing x_out (in-place frame update)
+    xa = x0.clone()
+    plan.reconstruct(dev(y1), xa, K, L, x_out=xa)
+    assert torch.equal(xa, x1)
+    plan.close()
+
+
+def test_edge_cases():
+    B = _B()
+    ng, J = 32, 3
+    y, mask = _frame(ng, J, 8, 1)
+    plan = B.Plan(ng, J, mask)
+    # zero Newton steps: x_out = x_0 = (1, 0), image = 0 (c = 0)
+    x, img = plan.reconstruct(dev(y), None, 0, 1)
+    xh = host(x)
+    assert np.all(xh[0] == 1) and np.all(xh[1:] == 0) and np.all(host(img) == 0)
+    # empty sampling pattern: b = 0 -> CG breakdown -> x stays x_0 exactly
+    plan.set_mask(np.zeros((ng, ng), np.uint8))
+    x, img = plan.reconstruct(dev(y), None, 2, 3)
+    xh = host(x)
+    assert np.all(xh[0] == 1) and np.all(xh[1:] == 0)
+    assert plan.stats()["cg_breakdown"]
+    plan.set_mask(mask)
+    # one CG iteration, one coil
+    plan1 = B.Plan(ng, 1, mask)
+    x, img = plan1.reconstruct(dev(y[:1]), None, 2, 1)
+    xo, io, _ = _oracle_recon(y[:1], mask, 2, 1)
+    assert rel(host(img), io) < 1e-4
+    # newton step 0 keeps rho == 1 bit-exactly (derived pin, oracle test_newton_step0_keeps_rho_bitexact)
+    x, _ = plan.reconstruct(dev(y), None, 1, 5)
+    assert np.all(host(x)[0] == 1)
+    # derivative before any set point is a state error
+    plan2 = B.Plan(ng, J, mask)
+    with pytest.raises(B.NlinvError) as e:
+        plan2.derivative(dev(np.zeros((J + 1, ng, ng))))
+    assert e.value.status == 3
+    for p in (plan, plan1, plan2):
+        p.close()
+
+
+def test_reconstruct_host_e2e_matches_device():
+    B = _B()
+    ng, J, K, L = 32, 4, 2, 5
+    y, mask = _frame(ng, J, 8, 1)
+    plan = B.Plan(ng, J, mask)
+    xd, imgd = plan.reconstruct(dev(y), None, K, L)
+    fr = torch.from_numpy(y).pin_memory()
+    xo = torch.empty(plan.x_shape, dtype=torch.complex64).pin_memory()
+    io = torch.empty(plan.image_shape, dtype=torch.complex64).pin_memory()
+    plan.reconstruct_host(fr, None, K, L, xo, io)
+    assert torch.equal(xo, xd.cpu()) and torch.equal(io, imgd.cpu())
+    plan.close()
+
+
+def test_reconstruct_c2_newton_step_full_size():
+    """BASELINE config 2 shape (12 coils, 384^2, 15 spokes, T=5) in bench's launch configuration,
+    one Newton step x 10 CG against the oracle."""
+    B = _B()
+    ng, J = 384, 12
+    y, mask = _frame(ng, J, 15, 5)
+    plan = B.Plan(ng, J, mask)
+    x, img = plan.reconstruct(dev(y), None, 1, 10)
+    xo, io, hist = _oracle_recon(y, mask, 1, 10)
+    assert rel(host(x), xo) < 1e-4
+    assert rel(host(img), io) < 1e-4
+    plan.close()
+
+
+@pytest.mark.slow
+def test_reconstruct_c2_full_frame():
+    """BASELINE config 2: the full 7 Newton x 10 CG frame vs the oracle (about a minute of CPU)."""
+    B = _B()
+    ng, J, K, L = 384, 12, 7, 10
+    y, mask = _frame(ng, J, 15, 5)
+    plan = B.Plan(ng, J, mask)
+    x, img = plan.reconstruct(dev(y), None, K, L)
+    xo, io, hist = _oracle_recon(y, mask, K, L)
+    assert rel(host(img), io) < 1e-3
+    st = plan.stats()
+    assert np.allclose(st["residual"], hist, rtol=1e-3)
+    plan.close()
