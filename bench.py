@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""NLINV frame-rate benchmark (BASELINE.json metric) through libnlinv.so's C ABI.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+For N > 1 launch with torch.distributed.run (one rank per GPU); coils are sharded over ranks
+(strong scaling, BASELINE config 3).
+
+A step = one full NLINV frame of BASELINE config 2: 12 coils, 384^2 grid (192^2 image), 15 radial
+spokes rotated over 5 turns, 7 Newton x 10 CG, the previous frame's x as prior.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+NG, J, SPOKES, TURNS, NEWTON, CG = 384, 12, 15, 5, 7, 10
+METRIC = "NLINV frames/sec and per-frame latency at 1/2/4/8 B200; % HBM roofline"
+WORKLOAD = ("C2: 12-coil 192x192 image on a 2x oversampled 384x384 grid, 15 radial spokes/frame "
+            "(5 turns), 7 Newton x 10 CG, frame stream with previous-frame prior")
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# Algorithmic (compulsory) bytes per launch, each operand read once and each result written once
+# at its minimal support. N = ng^2, Jl = local coils, c64 = 8 B.
+def algo_bytes(name: str, ng: int, Jl: int, it: int = 1, L: int = CG) -> float:
+    N = ng * ng
+    t = {
+        "col_ifft_w_cg": 28 * Jl * N + 4 * N + 24 * N,
+        "row_k2": 10 * Jl * N + 4 * N,
+        "col_psf": 8 * Jl * N + N,
+        "row_k4": 10 * Jl * N + 4 * N,
+        "col_fft_w_normal": 20 * Jl * N + 4 * N + 18 * N,   # + rho slice: S, p_rho in, Ap_rho out
+        "col_ifft_w": 8 * Jl * N + 4 * N + 4 * Jl * N,
+        "row_setpoint_fwd": 4 * Jl * N + 2 * Jl * N + 4 * Jl * N + 2 * N + 2 * N,
+        "row_setpoint": 4 * Jl * N + 2 * Jl * N + 4 * N,
+        "row_rss": 4 * Jl * N + 2 * Jl * N + 4 * N + 1 * N,
+        "col_resadj": 4 * Jl * N + 8 * Jl * N + N + 4 * Jl * N,
+        "col_fft_w_rhs": 4 * Jl * N + 8 * Jl * N + 8 * Jl * N + 4 * N + 16 * Jl * N + 34 * N,
+        "init_x": 8 * N * (Jl + 1),
+        "image": 2 * N + N + 2 * N,
+    }
+    if name == "frame":
+        # the persistent whole-frame kernel: every pass of the multi-kernel path, same bytes
+        K = NEWTON
+        newton = sum(algo_bytes(k, ng, Jl) for k in ("col_ifft_w", "row_setpoint_fwd", "col_resadj", "row_k4",
+                                                    "col_fft_w_rhs"))
+        cg = sum(algo_bytes(k, ng, Jl) for k in ("col_ifft_w_cg", "row_k2", "col_psf", "row_k4",
+                                                "col_fft_w_normal"))
+        upd = algo_bytes("cg_update", ng, Jl) * L
+        out = algo_bytes("col_ifft_w", ng, Jl) + algo_bytes("row_rss", ng, Jl) + algo_bytes("image", ng, Jl)
+        return K * (newton + L * cg + upd) + out
+    if name == "cg_update":
+        nb = Jl + 1
+        # iteration 0 skips the dx read; the last iteration only reads p, dx, x and writes x
+        per = [(40 if i == 0 else 48) if i < L - 1 else (24 if i == 0 else 32) for i in range(L)]
+        return statistics.mean(per) * N * nb
+    return float(t.get(name, 0.0))
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.p = None
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(device)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_frames(rank_first: int, count: int):
+    """T distinct synthetic frames (moving phantom, rotated spokes) for this rank's coils."""
+    import synth
+    from paper_1301_1215_b200 import radial_mask
+    frames, masks = [], []
+    for f in range(TURNS):
+        _, _, y = synth.frame_inputs(J, NG, t=f)
+        frames.append(np.ascontiguousarray(y[rank_first:rank_first + count].astype(np.complex64)))
+        masks.append(radial_mask(NG, SPOKES, TURNS, f))
+    return frames, masks
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1301_1215_b200 import Plan, get_unique_id
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    else:
+        nccl_id = None
+
+    from paper_1301_1215_b200 import radial_mask
+    mask0 = radial_mask(NG, SPOKES, TURNS, 0)
+    plan = Plan(NG, J, mask0, rank=rank, world=world, nccl_id=nccl_id)
+    frames, masks = make_frames(plan.first, plan.count)
+    dframes = [torch.from_numpy(f).cuda() for f in frames]
+    dmasks = [torch.from_numpy(m).cuda() for m in masks]
+    frame_dev = torch.empty_like(dframes[0])
+    x = torch.empty(plan.x_shape, dtype=torch.complex64, device="cuda")
+    img = torch.empty(plan.image_shape, dtype=torch.complex64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step(i, first):
+        frame_dev.copy_(dframes[i % TURNS])
+        plan.set_mask(dmasks[i % TURNS])
+        plan.reconstruct(frame_dev, None if first else x, NEWTON, CG, x_out=x, image_out=img)
+
+    # clocks are sampled from the start of warm-up through the end of the timed region
+    clocks = Clocks(local)
+    time.sleep(0.3)
+    # warm-up (also captures the CUDA graph of the warm-frame configuration)
+    step(0, True)
+    for i in range(max(args.warmup, 3)):
+        step(i + 1, False)
+    torch.cuda.synchronize()
+    barrier()
+
+    # timed region: K frames, L2 flushed before each, device time from CUDA events on the stream
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = plan.launch_count
+    torch.cuda.synchronize()
+    barrier()
+    for k in range(args.steps):
+        i = args.warmup + 1 + k
+        frame_dev.copy_(dframes[i % TURNS])
+        flush.zero_()
+        ev[k][0].record(stream)
+        plan.set_mask(dmasks[i % TURNS])
+        plan.reconstruct(frame_dev, x, NEWTON, CG, x_out=x, image_out=img)
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    clk["window"] = "warm-up + timed region"
+    launches = plan.launch_count - launches0
+    ms_steps = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(ms_steps)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    fps = args.steps / (total_ms / 1e3)
+
+    # end-to-end through the public streaming API: pinned host frame in, image out, every step
+    hframes = [torch.from_numpy(f).pin_memory() for f in frames]
+    hmasks = [torch.from_numpy(m).pin_memory() for m in masks]
+    himg = torch.empty(plan.image_shape, dtype=torch.complex64).pin_memory()
+    plan.stream_reset()
+    for i in range(max(args.warmup, 3) + 1):
+        plan.stream_frame(hframes[i % TURNS], hmasks[i % TURNS], NEWTON, CG, himg)
+    barrier()
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        i = k + 1
+        plan.stream_frame(hframes[i % TURNS], hmasks[i % TURNS], NEWTON, CG, himg)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d = frames[0].nbytes + masks[0].nbytes
+    d2h = himg.numel() * 8
+
+    # roofline: one profiled frame (every kernel bracketed by CUDA events on its stream)
+    plan.set_profiling(True)
+    step(args.warmup + 1 + args.steps, False)
+    prof = plan.profile()
+    plan.set_profiling(False)
+    peak, peak_src = _peaks()
+    frame_ms = sum(v["ms"] for v in prof.values())
+    top = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    tname, tv = top
+    if tname == "cg_update":
+        tb = algo_bytes(tname, NG, plan.count) * tv["launches"]
+    else:
+        tb = algo_bytes(tname, NG, plan.count) * tv["launches"]
+    achieved = tb / (tv["ms"] / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            tr = json.load(fh)
+        traffic = tr.get(tname, {}).get("dram_bytes_per_launch")
+    except Exception:
+        traffic = None
+    frame_bytes = sum(algo_bytes(k, NG, plan.count) * v["launches"] for k, v in prof.items())
+    kernels = {k: {"launches": v["launches"], "ms": round(v["ms"], 4),
+                   "share": round(v["ms"] / frame_ms, 4),
+                   "GBps": round(algo_bytes(k, NG, plan.count) * v["launches"] / (v["ms"] / 1e3) / 1e9, 1)}
+               for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
+
+    out = None
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(fps, 3), "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (modified Shepp-Logan + Gaussian coil maps, rasterised radial spokes)",
+            "config": {"workload": WORKLOAD, "ng": NG, "coils": J, "spokes": SPOKES, "turns": TURNS,
+                       "newton_steps": NEWTON, "cg_iters": CG, "coils_per_rank": plan.count,
+                       "parallelism": f"coil-sharded x{world}" if world > 1 else "single GPU",
+                       "l2": "flushed (256 MB write) before every timed frame, outside the events",
+                       "per_frame_ms": [round(m, 4) for m in ms_steps]},
+            "e2e": {"value": round(args.steps / e2e_s, 3), "unit": "frames/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "api": "nlinv_stream_frame (pinned host frame + mask in, image out)"},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "roofline": {"bound": "hbm", "kernel": tname, "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": tb / tv["launches"],
+                         "avg_launch_ms": tv["ms"] / tv["launches"],
+                         "share_of_frame": round(tv["ms"] / frame_ms, 4),
+                         "frame_algorithmic_GBps": round(frame_bytes / (frame_ms / 1e3) / 1e9, 1),
+                         "method": "one extra frame with every kernel bracketed by CUDA events (no graph)",
+                         "kernels": kernels},
+        }
+    plan.close()
+    return out, world, rank
+
+
+def oracle_sample(cg_iters=CG):
+    """The fp64 oracle on a bounded sample of the workload: Newton step 0 (cg_iters CG) of frame 0."""
+    import oracle as O
+    import synth
+    _, _, y = synth.frame_inputs(J, NG, t=0)
+    y = y.astype(np.complex64).astype(np.complex128)
+    P = O.radial_mask(NG, SPOKES, TURNS, 0).astype(np.float64)
+    winv, M = O.weights_inv(NG), O.fov_mask(NG)
+    x0 = O.initial_x(J, NG)
+    t0 = time.perf_counter()
+    O.newton_step(x0, x0, y, P, winv, M, 1.0, cg_iters)
+    return time.perf_counter() - t0
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands, on the host cores, same metric/config."""
+    world, rank, _ = _dist()
+    if rank != 0:
+        return None
+    for _ in range(args.warmup):
+        oracle_sample()
+    ts = [oracle_sample() for _ in range(args.steps)]
+    frame_s = NEWTON * statistics.mean(ts)   # each of the 7 Newton steps costs the same
+    fps = 1.0 / frame_s
+    sample = f"Newton step 0 of frame 0 (10 CG) of the C2 workload per step, frame time = 7 x mean step"
+    return {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": frame_s * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "ng": NG, "coils": J},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        out = run_reference(args)
+        if out is not None:
+            print(json.dumps(out))
+        return
+    out, world, rank = run_ours(args)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            t = oracle_sample()
+            fps = 1.0 / (NEWTON * t)
+            out["cpu_baseline"] = {"value": round(fps, 6), "unit": "frames/s", "cores": 1, "kind": "oracle",
+                                   "sample": f"Newton step 0 of frame 0 (10 CG) at C2 took {t:.2f} s; "
+                                             f"frame = 7 such steps"}
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

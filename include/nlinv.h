@@ -165,6 +165,24 @@ nlinv_status nlinv_reconstruct_host(nlinv_plan plan, const nlinv_c32* frame, con
                                     int newton_steps, int cg_iters, nlinv_c32* x_out,
                                     nlinv_c32* image_out, void* stream);
 
+/* Real-time streaming entry with HOST buffers (the call a scanner-side user makes per frame).
+ * frame_host: [count][ng][ng] k-space of the local coils (pinned memory for full speed).
+ * mask_host:  this frame's P_k, host uint8 [ng][ng], or NULL to keep the current one.
+ * image_host: [n][n] output (may be NULL).
+ * The plan keeps x on the device: the first frame after plan creation / nlinv_stream_reset starts
+ * from x_0 = x_ref = (1, 0); every later frame uses the previous frame's x as x_0 = x_ref, the
+ * temporal regularisation that makes frames sequential. Synchronises `stream`. */
+nlinv_status nlinv_stream_frame(nlinv_plan plan, const nlinv_c32* frame_host, const uint8_t* mask_host,
+                                int newton_steps, int cg_iters, nlinv_c32* image_host, void* stream);
+nlinv_status nlinv_stream_reset(nlinv_plan plan);
+
+/* Per-kernel timing: with profiling on, reconstruct/operator calls run without CUDA graphs and
+ * bracket every kernel with CUDA events on its stream. nlinv_plan_profile_json synchronises and
+ * writes {"kernel": [launches, total_ms], ...} into buf (ERR_SIZE if len is too small), then
+ * clears the record. */
+nlinv_status nlinv_plan_set_profiling(nlinv_plan plan, int on);
+nlinv_status nlinv_plan_profile_json(nlinv_plan plan, char* buf, size_t len);
+
 /* Statistics of the last reconstruct (synchronises the plan's last stream). */
 nlinv_status nlinv_plan_stats(nlinv_plan plan, nlinv_stats* out);
 

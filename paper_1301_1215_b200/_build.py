@@ -44,6 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "nvcc")
     nccl_inc, nccl_lib = _nccl_dirs()
     defs = ["-DNLINV_WITH_NCCL", "-I" + nccl_inc] if nccl_inc else []
+    defs += [d for d in os.environ.get("NLINV_DEFS", "").split() if d]
     digest = _sources_digest(" ".join(defs))
     stamp = LIB + ".sha256"
     if not force and os.path.exists(LIB) and os.path.exists(stamp) and open(stamp).read() == digest:

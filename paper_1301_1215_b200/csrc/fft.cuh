@@ -150,30 +150,34 @@ struct DFT<16, DIR> {
 // R0 == R_last wherever possible so inverse->pointwise->forward stays in registers.
 template <int L>
 struct Cfg;
-#define NLV_CFG(L_, E_, NP_, A_, B_, C_)                        \
+#define NLV_CFG(L_, E_, NP_, A_, B_, C_, D_)                    \
   template <>                                                   \
   struct Cfg<L_> {                                              \
     static constexpr int L = L_, E = E_, T = L_ / E_, NP = NP_; \
-    static constexpr int R0 = A_, R1 = B_, R2 = C_;             \
+    static constexpr int R0 = A_, R1 = B_, R2 = C_, R3 = D_;    \
   };
-NLV_CFG(16, 4, 2, 4, 4, 1)
-NLV_CFG(32, 8, 2, 8, 4, 1)
-NLV_CFG(48, 12, 2, 12, 4, 1)
-NLV_CFG(64, 8, 2, 8, 8, 1)
-NLV_CFG(96, 24, 2, 12, 8, 1)
-NLV_CFG(128, 16, 2, 16, 8, 1)
-NLV_CFG(192, 24, 3, 8, 3, 8)
-NLV_CFG(256, 16, 2, 16, 16, 1)
-NLV_CFG(384, 24, 3, 8, 6, 8)
-NLV_CFG(512, 16, 3, 8, 8, 8)
-NLV_CFG(768, 24, 3, 8, 12, 8)
-NLV_CFG(1024, 32, 3, 16, 4, 16)
+NLV_CFG(16, 4, 2, 4, 4, 1, 1)
+NLV_CFG(32, 8, 2, 8, 4, 1, 1)
+NLV_CFG(48, 12, 2, 12, 4, 1, 1)
+NLV_CFG(64, 8, 2, 8, 8, 1, 1)
+NLV_CFG(96, 24, 2, 12, 8, 1, 1)
+NLV_CFG(128, 16, 2, 16, 8, 1, 1)
+NLV_CFG(192, 24, 3, 8, 3, 8, 1)
+NLV_CFG(256, 16, 2, 16, 16, 1, 1)
+#ifdef NLV_E12_384
+NLV_CFG(384, 12, 4, 4, 4, 6, 4)
+#else
+NLV_CFG(384, 24, 3, 8, 6, 8, 1)
+#endif
+NLV_CFG(512, 16, 3, 8, 8, 8, 1)
+NLV_CFG(768, 24, 3, 8, 12, 8, 1)
+NLV_CFG(1024, 32, 3, 16, 4, 16, 1)
 #undef NLV_CFG
 
 template <int L>
 struct Sched {
   using C = Cfg<L>;
-  static constexpr int RL = (C::NP == 3) ? C::R2 : C::R1;  // radix of the last pass
+  static constexpr int RL = (C::NP == 4) ? C::R3 : (C::NP == 3) ? C::R2 : C::R1;  // radix of the last pass
   static constexpr bool kSymmetric = (C::R0 == RL);
   // index of register e in the pass-0 input pattern
   __device__ __forceinline__ static int in_idx(int t, int e) {
@@ -243,9 +247,13 @@ __device__ __forceinline__ void fft(float2* v, int t, const float2* tw, BUF& buf
   pass_compute<L, C::R0, 1, DIR>(v, t, tw);
   pass_exchange<L, C::R0, 1, C::R1>(v, t, buf, sync);
   pass_compute<L, C::R1, C::R0, DIR>(v, t, tw);
-  if constexpr (C::NP == 3) {
+  if constexpr (C::NP >= 3) {
     pass_exchange<L, C::R1, C::R0, C::R2>(v, t, buf, sync);
     pass_compute<L, C::R2, C::R0 * C::R1, DIR>(v, t, tw);
+  }
+  if constexpr (C::NP >= 4) {
+    pass_exchange<L, C::R2, C::R0 * C::R1, C::R3>(v, t, buf, sync);
+    pass_compute<L, C::R3, C::R0 * C::R1 * C::R2, DIR>(v, t, tw);
   }
 }
 

@@ -29,12 +29,6 @@ struct ColGeo {
   static constexpr size_t SMEM = sizeof(float2) * (size_t)L * (CW + 1) + 64 * sizeof(double);
 };
 
-template <int L>
-struct RowGeo {
-  static constexpr int T = Cfg<L>::T;
-  static constexpr int GCMAX = (L >= 512) ? 8 : 16;  // coil groups per CTA
-  static size_t smem(int gc) { return sizeof(float2) * (size_t)L * (gc + 1) + sizeof(float2) * (L / 2) + 64 * sizeof(double); }
-};
 
 struct SyncBlock {
   __device__ __forceinline__ void operator()() const { __syncthreads(); }
@@ -134,60 +128,96 @@ __device__ __forceinline__ float cg_gamma(const double* scal, int i) {
   return rr != 0.0 ? (float)(rr / pap) : 0.0f;
 }
 
-// ------------------------------------------------------------------ column kernels
+// ------------------------------------------------------------------ column task (one tile of CW columns)
+// Returns this thread's contributions to the (rho, chat) reductions of MODE. The caller owns
+// the twiddle table tw (shared) and the exchange buffer xb (shared, L*CW float2). Every thread
+// of the CTA must call it (the transform uses __syncthreads).
 template <int L, int MODE>
-__global__ void __launch_bounds__(ColGeo<L>::THREADS) col_kernel(ColArgs a, const float2* __restrict__ twg) {
+__device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, const float2* tw, float2* xb,
+                                         double& acc_rho, double& acc) {
   using C = Cfg<L>;
   using S = Sched<L>;
-  constexpr int T = C::T, E = C::E, CW = ColGeo<L>::CW, NT = ColGeo<L>::THREADS;
+  constexpr int T = C::T, E = C::E, CW = ColGeo<L>::CW;
   constexpr int n = L / 2, q = L / 4;
-  constexpr size_t N = (size_t)L * L, H = (size_t)n * L;
+  constexpr size_t N = (size_t)L * L, H = (size_t)n * L, Qs = (size_t)n * n;
   constexpr float invL = 1.0f / (float)L;
   constexpr int DIR_FIRST = (MODE == CK_IFFT_W || MODE == CK_IFFT_W_CG || MODE == CK_ADJ1) ? +1 : -1;
 
-  extern __shared__ float4 smem_raw[];
-  float2* tw = reinterpret_cast<float2*>(smem_raw);
-  float2* xb = tw + L;
-  double* red = reinterpret_cast<double*>(xb + (size_t)L * CW);
-
   const int tid = threadIdx.x, c = tid % CW, t = tid / CW;
-  const int x = blockIdx.x * CW + c;
-  const int j = blockIdx.y;
+  const int x = tile * CW + c;
 
   if constexpr (MODE == CK_IFFT_W_CG) {
     if (j == a.J) {  // rho-block slice of the fused CG direction update p = r + beta p
-      const float beta = cg_beta(a.scal, a.iter);
       for (int y = t; y < L; y += T) {
         const size_t i = (size_t)y * L + x;
         const float2 rv = a.rho_r[i], pv = a.rho_p[i];
-        a.rho_p[i] = make_float2(fmaf(beta, pv.x, rv.x), fmaf(beta, pv.y, rv.y));
+        a.rho_p[i] = make_float2(fmaf(a.beta, pv.x, rv.x), fmaf(a.beta, pv.y, rv.y));
       }
       return;
     }
   }
-  for (int i = tid; i < L; i += NT) tw[i] = twg[i];
-  __syncthreads();
+  if constexpr (MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ) {
+    if (j == a.J) {
+      // rho-block slice (replicated rho): out_rho = M . sum_s S_s (+ alpha p_rho | - alpha (rho - rho_ref))
+      const bool xin = (x >= q && x < q + n);
+      for (int y = t; y < L; y += T) {
+        const size_t i = (size_t)y * L + x;
+        float2 sv = make_float2(0.f, 0.f);
+        if (xin && y >= q && y < q + n) {
+          const size_t o = (size_t)(y - q) * n + (x - q);
+          for (int s = 0; s < a.nS; ++s) sv = cadd(sv, a.S[s * Qs + o]);   // ascending coil / rank order
+        }
+        if constexpr (MODE == CK_FFT_W_NORMAL) {
+          const float2 pv = a.rho_a[i];
+          const float2 o = make_float2(fmaf(a.alpha, pv.x, sv.x), fmaf(a.alpha, pv.y, sv.y));
+          a.rho_out[i] = o;
+          acc_rho += (double)pv.x * o.x + (double)pv.y * o.y;
+        } else if constexpr (MODE == CK_FFT_W_RHS) {
+          const float2 d = csub(a.rho_a[i], a.rho_b[i]);
+          const float2 b = make_float2(fmaf(-a.alpha, d.x, sv.x), fmaf(-a.alpha, d.y, sv.y));
+          a.rho_r[i] = b;
+          a.rho_p[i] = b;
+          acc_rho += (double)b.x * b.x + (double)b.y * b.y;
+        } else {
+          a.rho_out[i] = sv;
+        }
+      }
+      return;
+    }
+  }
 
   ColBuf<CW> buf{xb, c};
   float2 v[E];
-  double acc = 0.0;
 
   // ---------------- prologue: pass-0 input pattern, index = row
   if constexpr (MODE == CK_IFFT_W || MODE == CK_IFFT_W_CG) {
-    const float beta = (MODE == CK_IFFT_W_CG) ? cg_beta(a.scal, a.iter) : 0.0f;
+    constexpr int CH = 8;
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int yr = S::in_idx(t, e);
-      const size_t i = (size_t)yr * L + x;
-      float2 s;
-      if constexpr (MODE == CK_IFFT_W_CG) {
-        const float2 rv = a.r[j * N + i], pv = a.p[j * N + i];
-        s = make_float2(fmaf(beta, pv.x, rv.x), fmaf(beta, pv.y, rv.y));
-        a.p[j * N + i] = s;
-      } else {
-        s = a.src[j * N + i];
+    for (int e0 = 0; e0 < E; e0 += CH) {
+      float wv[CH];
+      float2 rv[CH], pv[CH];
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const size_t i = (size_t)S::in_idx(t, e0 + u) * L + x;
+        wv[u] = a.winv[i];
+        if constexpr (MODE == CK_IFFT_W_CG) {
+          rv[u] = a.r[j * N + i];
+          pv[u] = a.p[j * N + i];
+        } else {
+          rv[u] = a.src[j * N + i];
+        }
       }
-      v[e] = cscale(s, a.winv[i] * sgn_of(yr));
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const int yr = S::in_idx(t, e0 + u);
+        const size_t i = (size_t)yr * L + x;
+        float2 s = rv[u];
+        if constexpr (MODE == CK_IFFT_W_CG) {
+          s = make_float2(fmaf(a.beta, pv[u].x, rv[u].x), fmaf(a.beta, pv[u].y, rv[u].y));
+          a.p[j * N + i] = s;
+        }
+        v[e0 + u] = cscale(s, wv[u] * sgn_of(yr));
+      }
     }
   } else if constexpr (MODE == CK_ADJ1) {
 #pragma unroll
@@ -209,6 +239,13 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS) col_kernel(ColArgs a, cons
     }
   }
 
+  // mask bits of this thread's k-space rows, fetched before the transform (latency hidden)
+  uint32_t mbits = 0;
+  if constexpr (MODE == CK_PSF || MODE == CK_RESADJ || MODE == CK_FWDP) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) mbits |= (a.mask[(size_t)S::out_idx(t, e) * L + x] ? 1u : 0u) << e;
+  }
+
   fft<L, DIR_FIRST>(v, t, tw, buf, SyncBlock{});
 
   // ---------------- middle: k-space pointwise (registers hold output pattern, index = k)
@@ -216,15 +253,15 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS) col_kernel(ColArgs a, cons
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int k = S::out_idx(t, e);
-      const size_t i = (size_t)k * L + x;
+      const bool m = (mbits >> e) & 1u;
       if constexpr (MODE == CK_PSF) {
         // (-1)^k post-sign of the FFT and pre-sign of the IFFT cancel
-        v[e] = a.mask[i] ? v[e] : make_float2(0.f, 0.f);
+        v[e] = m ? v[e] : make_float2(0.f, 0.f);
       } else {
         // r = P (y - F x), F x = (-1)^k G; the IFFT consumes (-1)^k r = P((-1)^k y - G)
         float2 rr = make_float2(0.f, 0.f);
-        if (a.mask[i]) {
-          const float2 yv = cneg_if(a.y[j * N + i], k & 1);
+        if (m) {
+          const float2 yv = cneg_if(a.y[j * N + (size_t)k * L + x], k & 1);
           rr = csub(yv, v[e]);
           acc += (double)rr.x * rr.x + (double)rr.y * rr.y;
         }
@@ -249,45 +286,77 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS) col_kernel(ColArgs a, cons
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int k = S::out_idx(t, e);
-      const size_t i = (size_t)k * L + x;
-      a.out[j * N + i] = a.mask[i] ? cneg_if(v[e], k & 1) : make_float2(0.f, 0.f);
+      a.out[j * N + (size_t)k * L + x] = ((mbits >> e) & 1u) ? cneg_if(v[e], k & 1) : make_float2(0.f, 0.f);
     }
-  } else {  // CK_FFT_W_*
+  } else {  // CK_FFT_W_*: operands loaded in chunks so each chunk's loads are in flight together
+    constexpr int CH = 8;
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int k = S::out_idx(t, e);
-      const size_t i = (size_t)k * L + x;
-      const float2 val = cscale(v[e], a.winv[i] * sgn_of(k));
-      if constexpr (MODE == CK_FFT_W_NORMAL) {
-        const float2 pv = a.src2[j * N + i];
-        const float2 o = make_float2(fmaf(a.alpha, pv.x, val.x), fmaf(a.alpha, pv.y, val.y));
-        a.out[j * N + i] = o;
-        acc += (double)pv.x * o.x + (double)pv.y * o.y;
-      } else if constexpr (MODE == CK_FFT_W_RHS) {
-        const float2 xc = a.src[j * N + i], xr = a.src2[j * N + i];
-        const float2 d = csub(xc, xr);
-        const float2 b = make_float2(fmaf(-a.alpha, d.x, val.x), fmaf(-a.alpha, d.y, val.y));
-        a.r[j * N + i] = b;
-        a.p[j * N + i] = b;
-        acc += (double)b.x * b.x + (double)b.y * b.y;
-      } else {
-        a.out[j * N + i] = val;
+    for (int e0 = 0; e0 < E; e0 += CH) {
+      float wv[CH];
+      float2 o1[CH], o2[CH];
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const size_t i = (size_t)S::out_idx(t, e0 + u) * L + x;
+        wv[u] = a.winv[i];
+        if constexpr (MODE == CK_FFT_W_NORMAL) o1[u] = a.src2[j * N + i];
+        if constexpr (MODE == CK_FFT_W_RHS) {
+          o1[u] = a.src[j * N + i];
+          o2[u] = a.src2[j * N + i];
+        }
       }
-    }
-  }
-
-  if constexpr (MODE == CK_RESADJ || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS) {
-    if (a.partials != nullptr) {
-      const double vv[1] = {acc};
-      const int sl[1] = {a.out_slot};
-      grid_finish<1>(vv, a.partials, a.counter, a.scal_w, sl, red);
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const int k = S::out_idx(t, e0 + u);
+        const size_t i = (size_t)k * L + x;
+        const float2 val = cscale(v[e0 + u], wv[u] * sgn_of(k));
+        if constexpr (MODE == CK_FFT_W_NORMAL) {
+          const float2 pv = o1[u];
+          const float2 o = make_float2(fmaf(a.alpha, pv.x, val.x), fmaf(a.alpha, pv.y, val.y));
+          a.out[j * N + i] = o;
+          acc += (double)pv.x * o.x + (double)pv.y * o.y;
+        } else if constexpr (MODE == CK_FFT_W_RHS) {
+          const float2 d = csub(o1[u], o2[u]);
+          const float2 b = make_float2(fmaf(-a.alpha, d.x, val.x), fmaf(-a.alpha, d.y, val.y));
+          a.r[j * N + i] = b;
+          a.p[j * N + i] = b;
+          acc += (double)b.x * b.x + (double)b.y * b.y;
+        } else {
+          a.out[j * N + i] = val;
+        }
+      }
     }
   }
 }
 
-// ------------------------------------------------------------------ row kernels
 template <int L, int MODE>
-__global__ void __launch_bounds__(512) row_kernel(RowArgs a, const float2* __restrict__ twg) {
+__global__ void __launch_bounds__(ColGeo<L>::THREADS) col_kernel(ColArgs a, const float2* __restrict__ twg) {
+  constexpr int CW = ColGeo<L>::CW, NT = ColGeo<L>::THREADS;
+  extern __shared__ float4 smem_raw[];
+  float2* tw = reinterpret_cast<float2*>(smem_raw);
+  float2* xb = tw + L;
+  double* red = reinterpret_cast<double*>(xb + (size_t)L * CW);
+  for (int i = threadIdx.x; i < L; i += NT) tw[i] = twg[i];
+  __syncthreads();
+  if constexpr (MODE == CK_IFFT_W_CG) a.beta = cg_beta(a.scal, a.iter);
+  double acc_rho = 0.0, acc = 0.0;
+  // the rho slice (when present) is blockIdx.y == 0 so it is scheduled first
+  const bool has_rho = (MODE == CK_IFFT_W_CG || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ);
+  const int j = has_rho ? (blockIdx.y == 0 ? a.J : (int)blockIdx.y - 1) : (int)blockIdx.y;
+  col_task<L, MODE>(a, blockIdx.x, j, tw, xb, acc_rho, acc);
+  if constexpr (MODE == CK_RESADJ || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS) {
+    if (a.partials != nullptr) {
+      const double vv[2] = {acc_rho, acc};
+      const int sl[2] = {a.out_slot_rho, a.out_slot};
+      grid_finish<2>(vv, a.partials, a.counter, a.scal_w, sl, red);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ row task (one (coil, Omega row) per group)
+// Group g of the CTA (T threads) handles pair pair0 + g, pairs ordered coil-major (j * n + yy).
+// Groups are independent (each inside one warp); no CTA-wide barrier is used.
+template <int L, int MODE>
+__device__ __forceinline__ void row_task(const RowArgs& a, int pair0, const float2* tw, float2* xbase) {
   using C = Cfg<L>;
   using S = Sched<L>;
   constexpr int T = C::T, E = C::E;
@@ -295,118 +364,519 @@ __global__ void __launch_bounds__(512) row_kernel(RowArgs a, const float2* __res
   constexpr size_t H = (size_t)n * L, Q = (size_t)n * n;
   constexpr float invL = 1.0f / (float)L;
 
-  extern __shared__ float4 smem_raw[];
-  float2* tw = reinterpret_cast<float2*>(smem_raw);
-  float2* xbase = tw + L;                                  // [gc][L]
-  float2* accs = xbase + (size_t)L * a.gc;                 // [n] coil-sum accumulator
-
-  const int yy = blockIdx.x, row = q + yy;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int g = tid / T, t = tid % T;
+  const int g = threadIdx.x / T, t = threadIdx.x % T;
+  const int pair = pair0 + g;
+  const bool active = pair < a.J * n;
+  const int j = active ? pair / n : 0, yy = active ? pair % n : 0, row = q + yy;
   RowBuf buf{xbase + (size_t)g * L};
 
-  for (int i = tid; i < L; i += nt) tw[i] = twg[i];
-  if constexpr (MODE == RK_K4 || MODE == RK_RSS)
-    for (int i = tid; i < n; i += nt) accs[i] = make_float2(0.f, 0.f);
-  if constexpr (MODE == RK_SETPOINT || MODE == RK_SETPOINT_FWD || MODE == RK_RSS)
-    for (int i = tid; i < n; i += nt) a.rho_omega[yy * n + i] = a.xrho[(size_t)row * L + q + i];
-  __syncthreads();
+  if constexpr (MODE == RK_SETPOINT || MODE == RK_SETPOINT_FWD || MODE == RK_RSS) {
+    if (active && j == 0)
+      for (int i = t; i < n; i += T) a.rho_omega[(size_t)yy * n + i] = a.xrho[(size_t)row * L + q + i];
+  }
+  float2 v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int xi = S::in_idx(t, e);
+    v[e] = make_float2(0.f, 0.f);
+    if (active) v[e] = cneg_if(a.in[j * H + (size_t)yy * L + xi], xi & 1);
+  }
+  fft<L, +1>(v, t, tw, buf, SyncWarp{});
+  // v[e] now holds (-1)^k x (row IFFT), k = S::out_idx(t, e); only Omega columns are kept
 
-  for (int j0 = 0; j0 < a.J; j0 += a.gc) {
+  if constexpr (MODE == RK_SETPOINT || MODE == RK_SETPOINT_FWD || MODE == RK_RSS) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int k = S::out_idx(t, e);
+      if (out_is_omega<L>(e)) {
+        const float2 cv = cneg_if(v[e], k & 1);
+        if (active) a.c_omega[j * Q + (size_t)yy * n + (k - q)] = cv;
+        if constexpr (MODE == RK_SETPOINT_FWD) {
+          const float2 rv = active ? a.xrho[(size_t)row * L + k] : make_float2(0.f, 0.f);
+          v[e] = cscale(cmul(rv, cv), invL * sgn_of(k));
+        } else if constexpr (MODE == RK_RSS) {
+          if (active) a.rss[j * Q + (size_t)yy * n + (k - q)] = cv.x * cv.x + cv.y * cv.y;
+        }
+      } else {
+        v[e] = make_float2(0.f, 0.f);
+      }
+    }
+  } else if constexpr (MODE == RK_K2) {
+    float2 cv[E / 2], rv[E / 2], pr[E / 2];
+    int u = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (out_is_omega<L>(e)) {
+        const int k = S::out_idx(t, e);
+        if (active) {
+          cv[u] = a.c_omega[j * Q + (size_t)yy * n + (k - q)];
+          rv[u] = a.rho_omega[(size_t)yy * n + (k - q)];
+          pr[u] = a.prho[(size_t)row * L + k];
+        } else {
+          cv[u] = rv[u] = pr[u] = make_float2(0.f, 0.f);
+        }
+        ++u;
+      }
+    }
+    u = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (out_is_omega<L>(e)) {
+        const int k = S::out_idx(t, e);
+        const float2 dc = cneg_if(v[e], k & 1);
+        const float2 z = cadd(cmul(pr[u], cv[u]), cmul(rv[u], dc));
+        v[e] = cscale(z, invL * sgn_of(k));
+        ++u;
+      } else {
+        v[e] = make_float2(0.f, 0.f);
+      }
+    }
+  } else if constexpr (MODE == RK_K4) {
+    float2 cv[E / 2], rv[E / 2];
+    int u = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (out_is_omega<L>(e)) {
+        const int k = S::out_idx(t, e);
+        if (active) {
+          cv[u] = a.c_omega[j * Q + (size_t)yy * n + (k - q)];
+          rv[u] = a.rho_omega[(size_t)yy * n + (k - q)];
+        } else {
+          cv[u] = rv[u] = make_float2(0.f, 0.f);
+        }
+        ++u;
+      }
+    }
+    u = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (out_is_omega<L>(e)) {
+        const int k = S::out_idx(t, e);
+        const float2 uu = cneg_if(v[e], k & 1);
+        // per-coil term of sum_j conj(c_j) u_j (Table 1 "sum c_j"); summed in coil order by the consumer
+        if (active) a.S[j * Q + (size_t)yy * n + (k - q)] = cmulc(cv[u], uu);
+        v[e] = cscale(cmulc(rv[u], uu), invL * sgn_of(k));
+        ++u;
+      } else {
+        v[e] = make_float2(0.f, 0.f);
+      }
+    }
+  }
+
+  if constexpr (MODE == RK_SETPOINT_FWD || MODE == RK_K2 || MODE == RK_K4) {
+    out_to_in<L>(v, t, buf, SyncWarp{});
+    fft<L, -1>(v, t, tw, buf, SyncWarp{});
+    if (active) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int k = S::out_idx(t, e);
+        a.out[j * H + (size_t)yy * L + k] = cneg_if(v[e], k & 1);
+      }
+    }
+  }
+}
+
+// K4 as one CTA per Omega row over all local coils (chunks of GPC coils), so the channel sum
+// sum_j conj(c_j) u_j (Table 1 "sum c_j") is formed in shared memory in ascending coil order.
+template <int L, int GPC>
+__device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, const float2* tw, float2* xbase, float2* accs) {
+  using C = Cfg<L>;
+  using S = Sched<L>;
+  constexpr int T = C::T, E = C::E;
+  constexpr int n = L / 2, q = L / 4;
+  constexpr size_t H = (size_t)n * L, Q = (size_t)n * n;
+  constexpr float invL = 1.0f / (float)L;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int g = tid / T, t = tid % T;
+  const int row = q + yy;
+  RowBuf buf{xbase + (size_t)g * L};
+  for (int i = tid; i < n; i += nt) accs[i] = make_float2(0.f, 0.f);
+  // rho|Omega of this row is shared by every coil
+  float2 rv[E / 2];
+  {
+    int u = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (out_is_omega<L>(e)) rv[u++] = a.rho_omega[(size_t)yy * n + (S::out_idx(t, e) - q)];
+  }
+  for (int j0 = 0; j0 < a.J; j0 += GPC) {
     const int j = j0 + g;
     const bool active = j < a.J;
-    float2 v[E];
+    float2 v[E], cv[E / 2];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int xi = S::in_idx(t, e);
       v[e] = make_float2(0.f, 0.f);
       if (active) v[e] = cneg_if(a.in[j * H + (size_t)yy * L + xi], xi & 1);
     }
+    {
+      int u = 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (out_is_omega<L>(e)) {
+          cv[u] = active ? a.c_omega[j * Q + (size_t)yy * n + (S::out_idx(t, e) - q)] : make_float2(0.f, 0.f);
+          ++u;
+        }
+    }
     fft<L, +1>(v, t, tw, buf, SyncWarp{});
-    // v[e] now holds (-1)^k x (row IFFT), k = S::out_idx(t, e); only Omega columns are kept
-
-    if constexpr (MODE == RK_SETPOINT || MODE == RK_SETPOINT_FWD || MODE == RK_RSS) {
+    __syncthreads();  // accs / previous chunk's exchange buffers are free
+    {
+      int u = 0;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const int k = S::out_idx(t, e);
         if (out_is_omega<L>(e)) {
-          const float2 cv = cneg_if(v[e], k & 1);
-          if (active) a.c_omega[j * Q + (size_t)yy * n + (k - q)] = cv;
-          if constexpr (MODE == RK_SETPOINT_FWD) {
-            const float2 rv = a.xrho[(size_t)row * L + k];
-            v[e] = cscale(cmul(rv, cv), invL * sgn_of(k));
-          } else if constexpr (MODE == RK_RSS) {
-            buf(k - q) = make_float2(cv.x * cv.x + cv.y * cv.y, 0.f);
-          }
-        } else {
-          v[e] = make_float2(0.f, 0.f);
-        }
-      }
-    } else if constexpr (MODE == RK_K2) {
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int k = S::out_idx(t, e);
-        if (out_is_omega<L>(e) && active) {
-          const float2 dc = cneg_if(v[e], k & 1);
-          const float2 cv = a.c_omega[j * Q + (size_t)yy * n + (k - q)];
-          const float2 rv = a.rho_omega[(size_t)yy * n + (k - q)];
-          const float2 pr = a.prho[(size_t)row * L + k];
-          const float2 z = cadd(cmul(pr, cv), cmul(rv, dc));
-          v[e] = cscale(z, invL * sgn_of(k));
-        } else {
-          v[e] = make_float2(0.f, 0.f);
-        }
-      }
-    } else if constexpr (MODE == RK_K4) {
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int k = S::out_idx(t, e);
-        if (out_is_omega<L>(e)) {
-          const float2 u = cneg_if(v[e], k & 1);
-          float2 term = make_float2(0.f, 0.f);
-          if (active) {
-            const float2 cv = a.c_omega[j * Q + (size_t)yy * n + (k - q)];
-            term = cmulc(cv, u);
-          }
-          buf(k - q) = term;
-          const float2 rv = a.rho_omega[(size_t)yy * n + (k - q)];
-          v[e] = cscale(cmulc(rv, u), invL * sgn_of(k));
-        } else {
-          v[e] = make_float2(0.f, 0.f);
-        }
-      }
-    }
-
-    if constexpr (MODE == RK_K4 || MODE == RK_RSS) {
-      // ordered sum over the coils of this chunk (ascending coil index)
-      __syncthreads();
-      for (int xx = tid; xx < n; xx += nt) {
-        float2 s = accs[xx];
-        for (int gg = 0; gg < a.gc && j0 + gg < a.J; ++gg) s = cadd(s, xbase[(size_t)gg * L + xx]);
-        accs[xx] = s;
-      }
-      __syncthreads();
-    }
-
-    if constexpr (MODE == RK_SETPOINT_FWD || MODE == RK_K2 || MODE == RK_K4) {
-      out_to_in<L>(v, t, buf, SyncWarp{});
-      fft<L, -1>(v, t, tw, buf, SyncWarp{});
-      if (active) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
           const int k = S::out_idx(t, e);
-          a.out[j * H + (size_t)yy * L + k] = cneg_if(v[e], k & 1);
+          const float2 uu = cneg_if(v[e], k & 1);
+          buf(k - q) = cmulc(cv[u], uu);
+          v[e] = cscale(cmulc(rv[u], uu), invL * sgn_of(k));
+          ++u;
+        } else {
+          v[e] = make_float2(0.f, 0.f);
         }
+      }
+    }
+    __syncthreads();
+    for (int xx = tid; xx < n; xx += nt) {
+      float2 sacc = accs[xx];
+      for (int gg = 0; gg < GPC && j0 + gg < a.J; ++gg) sacc = cadd(sacc, xbase[(size_t)gg * L + xx]);
+      accs[xx] = sacc;
+    }
+    __syncthreads();
+    out_to_in<L>(v, t, buf, SyncWarp{});
+    fft<L, -1>(v, t, tw, buf, SyncWarp{});
+    if (active) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int k = S::out_idx(t, e);
+        a.out[j * H + (size_t)yy * L + k] = cneg_if(v[e], k & 1);
       }
     }
   }
+  __syncthreads();
+  for (int i = tid; i < n; i += nt) a.S[(size_t)yy * n + i] = accs[i];
+  __syncthreads();
+}
 
+template <int L>
+struct RowGeo {
+  static constexpr int T = Cfg<L>::T;
+  static constexpr int THREADS = 256;
+  static constexpr int GPC = THREADS / T;  // (coil, row) pairs per CTA
+  static constexpr size_t SMEM = sizeof(float2) * (size_t)L * (GPC + 1) + sizeof(float2) * (L / 2);
+};
+
+template <int L, int MODE>
+__global__ void __launch_bounds__(256) row_kernel(RowArgs a, const float2* __restrict__ twg) {
+  extern __shared__ float4 smem_raw[];
+  float2* tw = reinterpret_cast<float2*>(smem_raw);
+  float2* xb = tw + L;
+  for (int i = threadIdx.x; i < L; i += blockDim.x) tw[i] = twg[i];
+  __syncthreads();
+  if constexpr (MODE == RK_K4)
+    row_task_k4<L, RowGeo<L>::GPC>(a, blockIdx.x, tw, xb, xb + (size_t)L * RowGeo<L>::GPC);
+  else
+    row_task<L, MODE>(a, blockIdx.x * RowGeo<L>::GPC, tw, xb);
+}
+
+// ------------------------------------------------------------------ persistent frame kernel
+// One cooperative launch runs a whole frame (all Newton steps, all CG iterations) with grid
+// barriers between the passes, so the ~7 kernel boundaries per CG iteration (each a launch,
+// ramp-up and drain) become barriers and the twiddle table stays resident in shared memory.
+// Reductions: every CTA publishes (rho, chat) partials; after the barrier every CTA sums all
+// partials in CTA order itself (deterministic, no extra pass). world == 1 only (no NCCL inside).
+
+// Sense-reversing grid barrier over co-resident CTAs (cooperative launch guarantees residency).
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned nb = gridDim.x;
+    const unsigned g = *(volatile unsigned*)gen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == nb - 1) {
+      *count = 0u;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      unsigned spins = 0;
+      while (*(volatile unsigned*)gen == g) {
+        __nanosleep(20);
+        if (++spins > (1u << 28)) __trap();  // never hang the GPU: abort the context instead
+      }
+    }
+    __threadfence();  // acquire; gpu-scope fence also invalidates this SM's L1
+  }
+  __syncthreads();
+}
+
+// Publish this CTA's (rho, chat) partials to slot, barrier, and return the ordered totals.
+__device__ __forceinline__ double2 grid_reduce2(double vr, double vc, double* red_slot, unsigned* count,
+                                                unsigned* gen, double* sred) {
+  const double sr = block_sum(vr, sred);
+  const double sc = block_sum(vc, sred);
+  if (threadIdx.x == 0) {
+    red_slot[2 * blockIdx.x] = sr;
+    red_slot[2 * blockIdx.x + 1] = sc;
+  }
+  grid_barrier(count, gen);
+  __shared__ double2 tot;
+  if (threadIdx.x < 32) {
+    double ar = 0.0, ac = 0.0;
+    const volatile double* rs = red_slot;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) {
+      ar += rs[2 * b];
+      ac += rs[2 * b + 1];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ar += __shfl_xor_sync(0xffffffffu, ar, o);
+      ac += __shfl_xor_sync(0xffffffffu, ac, o);
+    }
+    if (threadIdx.x == 0) tot = make_double2(ar, ac);
+  }
+  __syncthreads();
+  return tot;
+}
+
+template <int L>
+struct FrameGeo {
+  static constexpr int NT = 256;
+  static constexpr bool kOk = (ColGeo<L>::THREADS == NT);  // 256-thread column tiles (ng >= 64, except 96)
+  static constexpr size_t SMEM_COL = sizeof(float2) * (size_t)L * ColGeo<L>::CW;
+  static constexpr size_t SMEM_ROW = sizeof(float2) * (size_t)L * RowGeo<L>::GPC + sizeof(float2) * (L / 2);
+  static constexpr size_t XB = SMEM_COL > SMEM_ROW ? SMEM_COL : SMEM_ROW;
+  static constexpr size_t SMEM = sizeof(float2) * L + XB + 64 * sizeof(double);
+};
+
+template <int L, int MODE>
+__device__ __forceinline__ void col_phase(const ColArgs& a, const float2* tw, float2* xb, int nslices,
+                                          double& acc_rho, double& acc) {
+  constexpr int NTILE = L / ColGeo<L>::CW;
+  const int ntask = NTILE * nslices;
+  for (int task = blockIdx.x; task < ntask; task += gridDim.x) {
+    // rho slice (j == J, when present) first: its tasks are longer than one coil tile
+    const int jj = task / NTILE, tile = task % NTILE;
+    const int j = (nslices > a.J) ? (jj == 0 ? a.J : jj - 1) : jj;
+    col_task<L, MODE>(a, tile, j, tw, xb, acc_rho, acc);
+    __syncthreads();  // the next task reuses xb
+  }
+}
+
+template <int L, int MODE>
+__device__ __forceinline__ void row_phase(const RowArgs& a, const float2* tw, float2* xb) {
+  constexpr int GPC = RowGeo<L>::GPC;
   if constexpr (MODE == RK_K4) {
-    __syncthreads();
-    for (int i = tid; i < n; i += nt) a.S[(size_t)yy * n + i] = accs[i];
-  } else if constexpr (MODE == RK_RSS) {
-    __syncthreads();
-    for (int i = tid; i < n; i += nt) a.rss[(size_t)yy * n + i] = accs[i].x;
+    for (int yy = blockIdx.x; yy < L / 2; yy += gridDim.x) row_task_k4<L, GPC>(a, yy, tw, xb, xb + (size_t)L * GPC);
+  } else {
+    const int ntask = (a.J * (L / 2) + GPC - 1) / GPC;
+    for (int task = blockIdx.x; task < ntask; task += gridDim.x) row_task<L, MODE>(a, task * GPC, tw, xb);
+  }
+}
+
+template <int L>
+__global__ void __launch_bounds__(256, 2) frame_kernel(FrameArgs f) {
+  constexpr int n = L / 2, q = L / 4;
+  constexpr size_t N = (size_t)L * L, Q = (size_t)n * n;
+  extern __shared__ float4 smem_raw[];
+  float2* tw = reinterpret_cast<float2*>(smem_raw);
+  float2* xb = tw + L;
+  double* sred = reinterpret_cast<double*>(reinterpret_cast<char*>(xb) + FrameGeo<L>::XB);
+  for (int i = threadIdx.x; i < L; i += blockDim.x) tw[i] = f.tw[i];
+  __syncthreads();
+
+  const int J = f.J;
+  ColArgs ca{};
+  ca.winv = f.winv;
+  ca.mask = f.mask;
+  ca.y = f.y;
+  ca.J = J;
+  ca.S = f.S_all;
+  ca.nS = 1;
+  RowArgs ra{};
+  ra.J = J;
+  ra.c_omega = f.c_omega;
+  ra.rho_omega = f.rho_omega;
+  ra.S = f.S_all;
+  ra.rss = f.rss_all;
+
+  double alpha_d = f.alpha0;
+  for (int nstep = 0; nstep < f.K; ++nstep, alpha_d *= f.q) {
+    const float alpha = (float)alpha_d;
+    double d0 = 0.0, d1 = 0.0;
+    // N1: c_j = W^-1 chat_j, column half
+    ca.src = f.x + N;
+    ca.out = f.tA;
+    col_phase<L, CK_IFFT_W>(ca, tw, xb, J, d0, d1);
+    grid_barrier(f.bar_count, f.bar_gen);
+    // N2: row half of c_j, c|Omega, rho|Omega, and the row FFT of rho c_j (forward operator)
+    ra.in = f.tA;
+    ra.out = f.tB;
+    ra.xrho = f.x;
+    row_phase<L, RK_SETPOINT_FWD>(ra, tw, xb);
+    grid_barrier(f.bar_count, f.bar_gen);
+    // N3: column FFT -> r = P (y - F x) (+ ||r||^2) -> column IFFT (adjoint head)
+    ca.in = f.tB;
+    ca.out = f.tA;
+    d0 = d1 = 0.0;
+    col_phase<L, CK_RESADJ>(ca, tw, xb, J, d0, d1);
+    double2 res = grid_reduce2(d0, d1, f.red + 0 * 2 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
+    if (blockIdx.x == 0 && threadIdx.x == 0) f.scal[SC_RES + nstep] = res.y;
+    // N4: row IFFT -> u, per-coil conj(c) u, conj(rho) u -> row FFT
+    ra.in = f.tA;
+    ra.out = f.tB;
+    row_phase<L, RK_K4>(ra, tw, xb);
+    grid_barrier(f.bar_count, f.bar_gen);
+    // N5: rhs b = DF^H r - alpha (x - x_ref); r = p = b
+    ca.in = f.tB;
+    ca.src = f.x + N;
+    ca.src2 = f.xref + N;
+    ca.r = f.r + N;
+    ca.p = f.p + N;
+    ca.rho_a = f.x;
+    ca.rho_b = f.xref;
+    ca.rho_r = f.r;
+    ca.rho_p = f.p;
+    ca.alpha = alpha;
+    d0 = d1 = 0.0;
+    col_phase<L, CK_FFT_W_RHS>(ca, tw, xb, J + 1, d0, d1);
+    double2 rr2 = grid_reduce2(d0, d1, f.red + 1 * 2 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
+    double rr = rr2.x + rr2.y, rr_prev = rr;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      f.scal[SC_RR_RHO] = rr2.x;
+      f.scal[SC_RR_CHAT] = rr2.y;
+    }
+    // CG
+    for (int it = 0; it < f.L; ++it) {
+      // P1: p = r + beta p (chat blocks + rho slice), t = w^-1 p -> column IFFT
+      ca.r = f.r + N;
+      ca.p = f.p + N;
+      ca.rho_r = f.r;
+      ca.rho_p = f.p;
+      ca.out = f.tA;
+      ca.beta = (it == 0 || rr_prev == 0.0) ? 0.0f : (float)(rr / rr_prev);
+      col_phase<L, CK_IFFT_W_CG>(ca, tw, xb, J + 1, d0, d1);
+      grid_barrier(f.bar_count, f.bar_gen);
+      // P2: K2
+      ra.in = f.tA;
+      ra.out = f.tB;
+      ra.prho = f.p;
+      row_phase<L, RK_K2>(ra, tw, xb);
+      grid_barrier(f.bar_count, f.bar_gen);
+      // P3: K3 (PSF convolution)
+      ca.in = f.tB;
+      ca.out = f.tA;
+      col_phase<L, CK_PSF>(ca, tw, xb, J, d0, d1);
+      grid_barrier(f.bar_count, f.bar_gen);
+      // P4: K4
+      ra.in = f.tA;
+      ra.out = f.tB;
+      row_phase<L, RK_K4>(ra, tw, xb);
+      grid_barrier(f.bar_count, f.bar_gen);
+      // P5: K5 + rho slice: Ap, <p, Ap>
+      ca.in = f.tB;
+      ca.src2 = f.p + N;
+      ca.out = f.Ap + N;
+      ca.rho_a = f.p;
+      ca.rho_out = f.Ap;
+      ca.alpha = alpha;
+      d0 = d1 = 0.0;
+      col_phase<L, CK_FFT_W_NORMAL>(ca, tw, xb, J + 1, d0, d1);
+      double2 pap = grid_reduce2(d0, d1, f.red + 2 * 2 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
+      const double papt = pap.x + pap.y;
+      const float gamma = (rr != 0.0) ? (float)(rr / papt) : 0.0f;
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        f.scal[SC_PAP_RHO + it] = pap.x;
+        f.scal[SC_PAP_CHAT + it] = pap.y;
+      }
+      // P6: dx += gamma p; r -= gamma Ap; <r, r>   (last iteration: x += dx + gamma p)
+      const bool last = (it == f.L - 1);
+      const long long n2 = (long long)N * (J + 1) / 2, nrho2 = (long long)N / 2;
+      const long long stride = (long long)gridDim.x * blockDim.x;
+      float4* p4 = reinterpret_cast<float4*>(f.p);
+      float4* dx4 = reinterpret_cast<float4*>(f.dx);
+      float4* r4 = reinterpret_cast<float4*>(f.r);
+      float4* x4 = reinterpret_cast<float4*>(f.x);
+      const float4* ap4 = reinterpret_cast<const float4*>(f.Ap);
+      double ar = 0.0, ac = 0.0;
+      for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += stride) {
+        const float4 pv = p4[i];
+        float4 d = (it > 0) ? dx4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        d.x = fmaf(gamma, pv.x, d.x); d.y = fmaf(gamma, pv.y, d.y);
+        d.z = fmaf(gamma, pv.z, d.z); d.w = fmaf(gamma, pv.w, d.w);
+        if (last) {
+          float4 xv = x4[i];
+          xv.x += d.x; xv.y += d.y; xv.z += d.z; xv.w += d.w;
+          x4[i] = xv;
+        } else {
+          dx4[i] = d;
+          const float4 av = ap4[i];
+          float4 rv = r4[i];
+          rv.x = fmaf(-gamma, av.x, rv.x); rv.y = fmaf(-gamma, av.y, rv.y);
+          rv.z = fmaf(-gamma, av.z, rv.z); rv.w = fmaf(-gamma, av.w, rv.w);
+          r4[i] = rv;
+          const double sq = (double)rv.x * rv.x + (double)rv.y * rv.y + (double)rv.z * rv.z + (double)rv.w * rv.w;
+          if (i < nrho2) ar += sq; else ac += sq;
+        }
+      }
+      if (!last) {
+        double2 r2 = grid_reduce2(ar, ac, f.red + 1 * 2 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
+        rr_prev = rr;
+        rr = r2.x + r2.y;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+          f.scal[SC_RR_RHO + it + 1] = r2.x;
+          f.scal[SC_RR_CHAT + it + 1] = r2.y;
+        }
+      } else {
+        grid_barrier(f.bar_count, f.bar_gen);
+      }
+    }
+  }
+  if (f.img != nullptr) {
+    double d0 = 0.0, d1 = 0.0;
+    ca.src = f.x + N;
+    ca.out = f.tA;
+    col_phase<L, CK_IFFT_W>(ca, tw, xb, J, d0, d1);
+    grid_barrier(f.bar_count, f.bar_gen);
+    ra.in = f.tA;
+    ra.xrho = f.x;
+    row_phase<L, RK_RSS>(ra, tw, xb);
+    grid_barrier(f.bar_count, f.bar_gen);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)Q;
+         i += (long long)gridDim.x * blockDim.x) {
+      float s = 0.f;
+      for (int jj = 0; jj < J; ++jj) s += f.rss_all[jj * Q + i];
+      f.img[i] = cscale(f.rho_omega[i], sqrtf(s));
+    }
+  }
+}
+
+template <int L>
+static cudaError_t launch_frame_l(const FrameArgs& f, cudaStream_t s) {
+  if constexpr (!FrameGeo<L>::kOk) {
+    return cudaErrorNotSupported;
+  } else {
+  auto kern = frame_kernel<L>;
+  const size_t smem = FrameGeo<L>::SMEM;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, FrameGeo<L>::NT, smem);
+  if (e != cudaSuccess) return e;
+  if (per < 1) return cudaErrorInvalidConfiguration;
+  int grid = nsm * (per > 2 ? 2 : per);
+  if (grid > kMaxFrameBlocks) grid = kMaxFrameBlocks;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(FrameGeo<L>::NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, f);
   }
 }
 
@@ -417,7 +887,8 @@ static cudaError_t launch_col_t(const ColArgs& a, const float2* tw, cudaStream_t
   const size_t smem = ColGeo<L>::SMEM;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int gy = (MODE == CK_IFFT_W_CG) ? a.J + 1 : a.J;
+  const int gy = (MODE == CK_IFFT_W_CG || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ)
+                     ? a.J + 1 : a.J;
   dim3 grid(L / ColGeo<L>::CW, gy);
   kern<<<grid, ColGeo<L>::THREADS, smem, s>>>(a, tw);
   return cudaGetLastError();
@@ -440,17 +911,13 @@ static cudaError_t launch_col_l(int mode, const ColArgs& a, const float2* tw, cu
 }
 
 template <int L, int MODE>
-static cudaError_t launch_row_t(const RowArgs& a0, const float2* tw, cudaStream_t s) {
-  RowArgs a = a0;
-  constexpr int T = Cfg<L>::T;
-  int gc = a.J < RowGeo<L>::GCMAX ? a.J : RowGeo<L>::GCMAX;
-  while ((gc * T) % 32 != 0) ++gc;  // whole warps
-  a.gc = gc;
-  const size_t smem = RowGeo<L>::smem(gc);
+static cudaError_t launch_row_t(const RowArgs& a, const float2* tw, cudaStream_t s) {
+  const size_t smem = RowGeo<L>::SMEM;
   auto kern = row_kernel<L, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<L / 2, gc * T, smem, s>>>(a, tw);
+  const int grid = (MODE == RK_K4) ? L / 2 : (a.J * (L / 2) + RowGeo<L>::GPC - 1) / RowGeo<L>::GPC;
+  kern<<<grid, RowGeo<L>::THREADS, smem, s>>>(a, tw);
   return cudaGetLastError();
 }
 
@@ -562,7 +1029,9 @@ static cudaError_t launch_fft2d_l(const float2* in, float2* out, int batch, int 
   cudaError_t launch_row_##L(int mode, const RowArgs& a, const float2* tw, cudaStream_t s);     \
   cudaError_t launch_fft2d_##L(const float2* in, float2* out, int batch, int inverse, const float2* tw, \
                                cudaStream_t s);                                                 \
-  int col_tiles_##L();
+  int col_tiles_##L();                                                                          \
+  cudaError_t launch_frame_##L(const FrameArgs& f, cudaStream_t s);                             \
+  bool frame_ok_##L();
 #define NLV_INSTANTIATE(L)                                                                       \
   cudaError_t launch_col_##L(int mode, const ColArgs& a, const float2* tw, cudaStream_t s) {    \
     return launch_col_l<L>(mode, a, tw, s);                                                      \
@@ -574,7 +1043,9 @@ static cudaError_t launch_fft2d_l(const float2* in, float2* out, int batch, int 
                                cudaStream_t s) {                                                 \
     return launch_fft2d_l<L>(in, out, batch, inverse, tw, s);                                    \
   }                                                                                              \
-  int col_tiles_##L() { return L / ColGeo<L>::CW; }
+  int col_tiles_##L() { return L / ColGeo<L>::CW; }                                             \
+  cudaError_t launch_frame_##L(const FrameArgs& f, cudaStream_t s) { return launch_frame_l<L>(f, s); } \
+  bool frame_ok_##L() { return FrameGeo<L>::kOk; }
 
 #define NLV_FOR_EACH_NG(X) X(16) X(32) X(48) X(64) X(96) X(128) X(192) X(256) X(384) X(512) X(768) X(1024)
 NLV_FOR_EACH_NG(NLV_DECLARE)

@@ -56,8 +56,11 @@ struct nlinv_plan_s {
   // workspace
   float2 *xref = nullptr, *dx = nullptr, *r = nullptr, *p = nullptr, *Ap = nullptr;
   float2 *tA = nullptr, *tB = nullptr, *c_omega = nullptr, *rho_omega = nullptr;
-  float2 *S = nullptr, *S_sum = nullptr;
-  float *rss = nullptr, *rss_sum = nullptr;
+  float2 *S_all = nullptr, *S = nullptr, *S_sum = nullptr;   // per-coil terms; local sum; rank sum
+  float *rss_all = nullptr, *rss = nullptr, *rss_sum = nullptr;
+  double* fred = nullptr;        // frame-kernel reduction partials
+  unsigned* fbar = nullptr;      // frame-kernel grid barrier (count, generation)
+  bool use_frame = false;
   double *scal = nullptr, *partials = nullptr;
   unsigned* counter = nullptr;
   // host e2e staging (device side)
@@ -68,6 +71,25 @@ struct nlinv_plan_s {
   long long gkernels = 0;
   cudaStream_t last_stream = nullptr;
   int last_K = 0, last_L = 0;
+  // streaming state (nlinv_stream_frame)
+  bool stream_started = false;
+  // per-kernel event profiling (nlinv_plan_set_profiling)
+  struct ProfRec {
+    const char* name;
+    cudaEvent_t e0, e1;
+  };
+  bool prof = false;
+  std::vector<ProfRec> prof_rec;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  cudaEvent_t event() {
+    if (ev_used == ev_pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_used++];
+  }
 #ifdef NLINV_WITH_NCCL
   ncclComm_t comm = nullptr;
 #endif
@@ -198,14 +220,14 @@ extern "C" nlinv_status nlinv_coil_partition(int ncoils, int world, int rank, in
 // ------------------------------------------------------------------ plan
 static void plan_free(nlinv_plan pl) {
   if (!pl) return;
-  if (pl->S_sum == pl->S) pl->S_sum = nullptr;
-  if (pl->rss_sum == pl->rss) pl->rss_sum = nullptr;
   void* ptrs[] = {pl->tw, pl->winv, pl->mask, pl->xref, pl->dx, pl->r, pl->p, pl->Ap, pl->tA, pl->tB,
-                  pl->c_omega, pl->rho_omega, pl->S, pl->S_sum, pl->rss, pl->rss_sum, pl->scal, pl->partials,
+                  pl->c_omega, pl->rho_omega, pl->S_all, pl->S, pl->S_sum, pl->rss_all, pl->rss, pl->rss_sum,
+                  pl->fred, pl->fbar, pl->scal, pl->partials,
                   pl->counter, pl->h_frame, pl->h_x, pl->h_img};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
+  for (cudaEvent_t e : pl->ev_pool) cudaEventDestroy(e);
 #ifdef NLINV_WITH_NCCL
   if (pl->comm) ncclCommDestroy(pl->comm);
 #endif
@@ -271,10 +293,16 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
   ok &= alloc((void**)&pl->c_omega, sizeof(float2) * pl->Q * pl->J);
   ok &= alloc((void**)&pl->rho_omega, sizeof(float2) * pl->Q);
   ok &= alloc((void**)&pl->S, sizeof(float2) * pl->Q);
-  ok &= alloc((void**)&pl->rss, sizeof(float) * pl->Q);
+  ok &= alloc((void**)&pl->rss_all, sizeof(float) * pl->Q * pl->J);
   if (pl->world > 1) {
+    ok &= alloc((void**)&pl->rss, sizeof(float) * pl->Q);
     ok &= alloc((void**)&pl->S_sum, sizeof(float2) * pl->Q);
     ok &= alloc((void**)&pl->rss_sum, sizeof(float) * pl->Q);
+  }
+  pl->use_frame = (pl->world == 1) && frame_supported(nx) && std::getenv("NLINV_NO_FRAME") == nullptr;
+  if (pl->use_frame) {
+    ok &= alloc((void**)&pl->fred, sizeof(double) * 3 * 2 * kMaxFrameBlocks);
+    ok &= alloc((void**)&pl->fbar, sizeof(unsigned) * 2);
   }
   ok &= alloc((void**)&pl->scal, sizeof(double) * SC_TOTAL);
   ok &= alloc((void**)&pl->partials, sizeof(double) * 2 * kMaxRedBlocks);
@@ -283,10 +311,6 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
     plan_free(pl);
     cudaGetLastError();
     return fail(nullptr, NLINV_ERR_NOMEM, "device allocation failed");
-  }
-  if (pl->world == 1) {
-    pl->S_sum = pl->S;
-    pl->rss_sum = pl->rss;
   }
   // one-time tables in fp64, rounded to fp32 (R2): twiddles e^{-2 pi i m / ng}, w^{-1}(k)
   std::vector<float2> tw(nx);
@@ -309,6 +333,7 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
   if (e == cudaSuccess) e = cudaMemcpy(pl->mask, m8.data(), N, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(pl->scal, 0, sizeof(double) * SC_TOTAL);
   if (e == cudaSuccess) e = cudaMemset(pl->counter, 0, sizeof(unsigned) * 4);
+  if (e == cudaSuccess && pl->fbar) e = cudaMemset(pl->fbar, 0, sizeof(unsigned) * 2);
   if (e != cudaSuccess) {
     std::string msg = std::string("plan upload: ") + cudaGetErrorString(e);
     plan_free(pl);
@@ -364,11 +389,33 @@ extern "C" long long nlinv_plan_launch_count(nlinv_plan pl) { return pl ? pl->la
 // ------------------------------------------------------------------ enqueue helpers
 namespace {
 
+const char* kColNames[] = {"col_ifft_w", "col_ifft_w_cg", "col_fwdp", "col_psf", "col_resadj", "col_adj1",
+                           "col_fft_w_normal", "col_fft_w_rhs", "col_fft_w_adj"};
+const char* kRowNames[] = {"row_setpoint", "row_setpoint_fwd", "row_rss", "row_k2", "row_k4"};
+
 struct Enq {
   nlinv_plan pl;
   cudaStream_t s;
   long long kernels = 0;
 
+  // launch one kernel; with profiling on, bracket it with events on its own stream
+  template <class F>
+  nlinv_status kern(const char* name, F&& launch) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (pl->prof) {
+      e0 = pl->event();
+      cudaEventRecord(e0, s);
+    }
+    cudaError_t e = launch();
+    if (pl->prof) {
+      e1 = pl->event();
+      cudaEventRecord(e1, s);
+      pl->prof_rec.push_back({name, e0, e1});
+    }
+    ++kernels;
+    if (e != cudaSuccess) return fail(pl, NLINV_ERR_CUDA, std::string(name) + ": " + cudaGetErrorString(e));
+    return NLINV_OK;
+  }
   nlinv_status col(int mode, ColArgs a) {
     a.winv = pl->winv;
     a.mask = pl->mask;
@@ -376,19 +423,13 @@ struct Enq {
     a.scal_w = pl->scal;
     a.counter = pl->counter;
     a.J = pl->J;
-    cudaError_t e = launch_col(pl->ng, mode, a, pl->tw, s);
-    ++kernels;
-    if (e != cudaSuccess) return fail(pl, NLINV_ERR_CUDA, std::string("col kernel: ") + cudaGetErrorString(e));
-    return NLINV_OK;
+    return kern(kColNames[mode], [&] { return launch_col(pl->ng, mode, a, pl->tw, s); });
   }
   nlinv_status row(int mode, RowArgs a) {
     a.J = pl->J;
     a.c_omega = pl->c_omega;
     a.rho_omega = pl->rho_omega;
-    cudaError_t e = launch_row(pl->ng, mode, a, pl->tw, s);
-    ++kernels;
-    if (e != cudaSuccess) return fail(pl, NLINV_ERR_CUDA, std::string("row kernel: ") + cudaGetErrorString(e));
-    return NLINV_OK;
+    return kern(kRowNames[mode], [&] { return launch_row(pl->ng, mode, a, pl->tw, s); });
   }
   VecArgs vec() const {
     VecArgs v{};
@@ -400,8 +441,8 @@ struct Enq {
     v.ntot = (long long)pl->N * (1 + pl->J);
     return v;
   }
+  // a stream operation that is not a kernel (memcpy)
   nlinv_status check(cudaError_t e, const char* what) {
-    ++kernels;
     if (e != cudaSuccess) return fail(pl, NLINV_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
     return NLINV_OK;
   }
@@ -468,7 +509,8 @@ nlinv_status enq_derivative_head(Enq& q, const float2* dx, bool cg_fused, int it
   return NLINV_OK;
 }
 
-// K4 on tA -> tB and the coil sum S, then the block-wise all-reduce of P:246 / P:289
+// K4 on tA -> tB and the per-coil terms conj(c_j) u_j; for world > 1 the local coil sum is
+// all-reduced over ranks (the block-wise all-reduce of P:246 / P:289, out of place).
 nlinv_status enq_k4_allreduce(Enq& q) {
   nlinv_plan pl = q.pl;
   RowArgs ra{};
@@ -480,6 +522,12 @@ nlinv_status enq_k4_allreduce(Enq& q) {
   return NLINV_OK;
 }
 
+// the coil-sum plane the rho slices read (local, or rank-summed for world > 1)
+void set_S(nlinv_plan pl, ColArgs& c) {
+  c.S = (pl->world > 1) ? pl->S_sum : pl->S;
+  c.nS = 1;
+}
+
 // out = (DF^H DF + alpha) dx; with_cg: the CG-fused variant on the plan's p (iteration iter)
 nlinv_status enq_normal(Enq& q, float alpha, const float2* dx, float2* out, bool cg, int iter) {
   nlinv_plan pl = q.pl;
@@ -489,20 +537,17 @@ nlinv_status enq_normal(Enq& q, float alpha, const float2* dx, float2* out, bool
   ca.out = pl->tA;
   TRY(q.col(CK_PSF, ca));
   TRY(enq_k4_allreduce(q));
-  VecArgs va = q.vec();
-  va.S = pl->S_sum;
-  va.p = const_cast<float2*>(dx);
-  va.out = out;
-  va.alpha = alpha;
-  va.iter = iter;
-  TRY(q.check(launch_rho_finish(pl->ng, va, cg ? 1 : 0, q.s), "rho_finish"));
   ColArgs cb{};
   cb.in = pl->tB;
   cb.src2 = dx + pl->N;
   cb.out = out + pl->N;
+  set_S(pl, cb);
+  cb.rho_a = dx;
+  cb.rho_out = out;
   cb.alpha = alpha;
   cb.partials = cg ? pl->partials : nullptr;
   cb.out_slot = SC_PAP_CHAT + iter;
+  cb.out_slot_rho = SC_PAP_RHO + iter;
   TRY(q.col(CK_FFT_W_NORMAL, cb));
   if (cg) TRY(q.allreduce_scalar(SC_PAP_CHAT + iter));
   return NLINV_OK;
@@ -519,8 +564,39 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
     if (prior != x)
       TRY(q.check(cudaMemcpyAsync(x, prior, tot * sizeof(float2), cudaMemcpyDeviceToDevice, q.s), "copy prior"));
   } else {
-    TRY(q.check(launch_init_x(pl->xref, (long long)N, (long long)tot, q.s), "init_x"));
-    TRY(q.check(launch_init_x(x, (long long)N, (long long)tot, q.s), "init_x"));
+    TRY(q.kern("init_x", [&] { return launch_init_x(pl->xref, (long long)N, (long long)tot, q.s); }));
+    TRY(q.kern("init_x", [&] { return launch_init_x(x, (long long)N, (long long)tot, q.s); }));
+  }
+  if (pl->use_frame && K > 0) {
+    // one cooperative launch for the whole frame (all Newton steps, CG iterations, output)
+    FrameArgs f{};
+    f.x = x;
+    f.xref = pl->xref;
+    f.dx = pl->dx;
+    f.r = pl->r;
+    f.p = pl->p;
+    f.Ap = pl->Ap;
+    f.tA = pl->tA;
+    f.tB = pl->tB;
+    f.c_omega = pl->c_omega;
+    f.rho_omega = pl->rho_omega;
+    f.S_all = pl->S;
+    f.rss_all = pl->rss_all;
+    f.img = img;
+    f.y = frame;
+    f.winv = pl->winv;
+    f.mask = pl->mask;
+    f.tw = pl->tw;
+    f.scal = pl->scal;
+    f.red = pl->fred;
+    f.bar_count = pl->fbar;
+    f.bar_gen = pl->fbar + 1;
+    f.J = pl->J;
+    f.K = K;
+    f.L = L;
+    f.alpha0 = pl->prm.alpha0;
+    f.q = pl->prm.q;
+    return q.kern("frame", [&] { return launch_frame(pl->ng, f, q.s); });
   }
   double alpha_d = pl->prm.alpha0;
   for (int nstep = 0; nstep < K; ++nstep, alpha_d *= pl->prm.q) {
@@ -547,15 +623,13 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
     cb.alpha = alpha;
     cb.partials = pl->partials;
     cb.out_slot = SC_RR_CHAT + 0;
+    cb.out_slot_rho = SC_RR_RHO + 0;
+    set_S(pl, cb);
+    cb.rho_a = x;
+    cb.rho_b = pl->xref;
+    cb.rho_r = pl->r;
+    cb.rho_p = pl->p;
     TRY(q.col(CK_FFT_W_RHS, cb));
-    VecArgs vr = q.vec();
-    vr.S = pl->S_sum;
-    vr.x = x;
-    vr.xref = pl->xref;
-    vr.r = pl->r;
-    vr.p = pl->p;
-    vr.alpha = alpha;
-    TRY(q.check(launch_rho_rhs(pl->ng, vr, q.s), "rho_rhs"));
     TRY(q.allreduce_scalar(SC_RR_CHAT + 0));
     // CG: L iterations of the normal operator + vector updates
     for (int it = 0; it < L; ++it) {
@@ -568,7 +642,7 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
       vu.Ap = pl->Ap;
       vu.iter = it;
       vu.last = (it == L - 1);
-      TRY(q.check(launch_cg_update(pl->ng, vu, q.s), "cg_update"));
+      TRY(q.kern("cg_update", [&] { return launch_cg_update(pl->ng, vu, q.s); }));
       if (!vu.last) TRY(q.allreduce_scalar(SC_RR_CHAT + it + 1));
     }
   }
@@ -580,10 +654,15 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
     RowArgs ra{};
     ra.in = pl->tA;
     ra.xrho = x;
-    ra.rss = pl->rss;
+    ra.rss = pl->rss_all;
     TRY(q.row(RK_RSS, ra));
-    TRY(q.allreduce_f(pl->rss, pl->rss_sum, pl->Q));
-    TRY(q.check(launch_image(pl->ng, pl->rho_omega, pl->rss_sum, img, q.s), "image"));
+    if (pl->world > 1) {
+      TRY(q.kern("rss_sum", [&] { return launch_rss_sum(pl->ng, pl->rss_all, pl->J, pl->rss, q.s); }));
+      TRY(q.allreduce_f(pl->rss, pl->rss_sum, pl->Q));
+      TRY(q.kern("image", [&] { return launch_image(pl->ng, pl->rho_omega, pl->rss_sum, 1, img, q.s); }));
+    } else {
+      TRY(q.kern("image", [&] { return launch_image(pl->ng, pl->rho_omega, pl->rss_all, pl->J, img, q.s); }));
+    }
   }
   return NLINV_OK;
 }
@@ -643,11 +722,9 @@ extern "C" nlinv_status nlinv_apply_adjoint(nlinv_plan pl, const nlinv_c32* dy, 
     ColArgs cb{};
     cb.in = pl->tB;
     cb.out = (float2*)dx + pl->N;
+    set_S(pl, cb);
+    cb.rho_out = (float2*)dx;
     TRY(q.col(CK_FFT_W_ADJ, cb));
-    VecArgs va = q.vec();
-    va.S = pl->S_sum;
-    va.out = (float2*)dx;
-    TRY(q.check(launch_rho_adj(pl->ng, va, q.s), "rho_adj"));
     return NLINV_OK;
   };
   nlinv_status st = body();
@@ -696,7 +773,7 @@ extern "C" nlinv_status nlinv_reconstruct(nlinv_plan pl, const nlinv_c32* frame,
   key.K = newton_steps;
   key.L = cg_iters;
   key.stream = s;
-  const bool use_graph = (s != nullptr) && (std::getenv("NLINV_NO_GRAPH") == nullptr);
+  const bool use_graph = (s != nullptr) && !pl->prof && (std::getenv("NLINV_NO_GRAPH") == nullptr);
   if (use_graph && pl->gexec && pl->gkey == key) {
     CU(cudaGraphLaunch(pl->gexec, s));
     pl->launches += pl->gkernels;
@@ -775,5 +852,77 @@ extern "C" nlinv_status nlinv_plan_stats(nlinv_plan pl, nlinv_stats* out) {
     if (sc[SC_RR_RHO + i] + sc[SC_RR_CHAT + i] == 0.0) out->cg_breakdown = 1;
   for (int k = 1; k < pl->last_K && k < 64; ++k)
     if (out->residual[k] > 10.0 * out->residual[0]) out->diverged = 1;
+  return NLINV_OK;
+}
+
+// ------------------------------------------------------------------ streaming (real-time) entry
+extern "C" nlinv_status nlinv_stream_reset(nlinv_plan pl) {
+  if (!pl) return fail(pl, NLINV_ERR_ARG, "NULL plan");
+  pl->stream_started = false;
+  return NLINV_OK;
+}
+
+extern "C" nlinv_status nlinv_stream_frame(nlinv_plan pl, const nlinv_c32* frame_host, const uint8_t* mask_host,
+                                           int newton_steps, int cg_iters, nlinv_c32* image_host, void* stream) {
+  if (!pl || !frame_host) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  const size_t N = pl->N, tot = N * (1 + pl->J);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!pl->h_frame) {
+    CU(cudaMalloc((void**)&pl->h_frame, sizeof(float2) * N * pl->J));
+    CU(cudaMalloc((void**)&pl->h_x, sizeof(float2) * tot));
+    CU(cudaMalloc((void**)&pl->h_img, sizeof(float2) * pl->Q));
+  }
+  CU(cudaMemcpyAsync(pl->h_frame, frame_host, sizeof(float2) * N * pl->J, cudaMemcpyHostToDevice, s));
+  if (mask_host) CU(cudaMemcpyAsync(pl->mask, mask_host, N, cudaMemcpyHostToDevice, s));
+  nlinv_status st = nlinv_reconstruct(pl, (const nlinv_c32*)pl->h_frame,
+                                      pl->stream_started ? (const nlinv_c32*)pl->h_x : nullptr, newton_steps,
+                                      cg_iters, (nlinv_c32*)pl->h_x, image_host ? (nlinv_c32*)pl->h_img : nullptr,
+                                      stream);
+  if (st != NLINV_OK) return st;
+  pl->stream_started = true;
+  if (image_host) CU(cudaMemcpyAsync(image_host, pl->h_img, sizeof(float2) * pl->Q, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return NLINV_OK;
+}
+
+// ------------------------------------------------------------------ per-kernel profiling
+extern "C" nlinv_status nlinv_plan_set_profiling(nlinv_plan pl, int on) {
+  if (!pl) return fail(pl, NLINV_ERR_ARG, "NULL plan");
+  pl->prof = on != 0;
+  pl->prof_rec.clear();
+  pl->ev_used = 0;
+  return NLINV_OK;
+}
+
+extern "C" nlinv_status nlinv_plan_profile_json(nlinv_plan pl, char* buf, size_t len) {
+  if (!pl || !buf || len == 0) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  CU(cudaDeviceSynchronize());
+  std::vector<std::string> names;
+  std::vector<double> ms;
+  std::vector<long long> cnt;
+  for (const auto& r : pl->prof_rec) {
+    float t = 0.f;
+    CU(cudaEventElapsedTime(&t, r.e0, r.e1));
+    size_t k = 0;
+    while (k < names.size() && names[k] != r.name) ++k;
+    if (k == names.size()) {
+      names.push_back(r.name);
+      ms.push_back(0.0);
+      cnt.push_back(0);
+    }
+    ms[k] += t;
+    cnt[k] += 1;
+  }
+  std::string out = "{";
+  for (size_t k = 0; k < names.size(); ++k) {
+    char tmp[160];
+    std::snprintf(tmp, sizeof(tmp), "%s\"%s\": [%lld, %.6f]", k ? ", " : "", names[k].c_str(), cnt[k], ms[k]);
+    out += tmp;
+  }
+  out += "}";
+  pl->prof_rec.clear();
+  pl->ev_used = 0;
+  if (out.size() + 1 > len) return fail(pl, NLINV_ERR_SIZE, "profile buffer too small");
+  std::memcpy(buf, out.c_str(), out.size() + 1);
   return NLINV_OK;
 }

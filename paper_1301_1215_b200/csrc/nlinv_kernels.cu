@@ -7,86 +7,56 @@ namespace nlv {
 // ------------------------------------------------------------------ rho-block kernels
 constexpr int kVecThreads = 256;
 
-// Ap_rho = M . S + alpha p_rho (whole grid), <p_rho, Ap_rho> partial
-__global__ void __launch_bounds__(kVecThreads) rho_finish_kernel(VecArgs a, int L, int with_dot) {
-  __shared__ double red[32];
-  const int n = L / 2, q = L / 4;
-  double acc = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.nrho; i += (long long)gridDim.x * blockDim.x) {
-    const int y = (int)(i / L), xx = (int)(i % L);
-    float2 s = make_float2(0.f, 0.f);
-    if (y >= q && y < q + n && xx >= q && xx < q + n) s = a.S[(size_t)(y - q) * n + (xx - q)];
-    const float2 pv = a.p[i];
-    const float2 o = make_float2(fmaf(a.alpha, pv.x, s.x), fmaf(a.alpha, pv.y, s.y));
-    a.out[i] = o;
-    acc += (double)pv.x * o.x + (double)pv.y * o.y;
-  }
-  if (with_dot) {
-    const double vv[1] = {acc};
-    const int sl[1] = {SC_PAP_RHO + a.iter};
-    grid_finish<1>(vv, a.partials, a.counter, a.scal_w, sl, red);
-  }
-}
-
-// b_rho = M . S - alpha (rho - rho_ref); r = p = b; <b, b> partial
-__global__ void __launch_bounds__(kVecThreads) rho_rhs_kernel(VecArgs a, int L) {
-  __shared__ double red[32];
-  const int n = L / 2, q = L / 4;
-  double acc = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.nrho; i += (long long)gridDim.x * blockDim.x) {
-    const int y = (int)(i / L), xx = (int)(i % L);
-    float2 s = make_float2(0.f, 0.f);
-    if (y >= q && y < q + n && xx >= q && xx < q + n) s = a.S[(size_t)(y - q) * n + (xx - q)];
-    const float2 d = csub(a.x[i], a.xref[i]);
-    const float2 b = make_float2(fmaf(-a.alpha, d.x, s.x), fmaf(-a.alpha, d.y, s.y));
-    a.r[i] = b;
-    a.p[i] = b;
-    acc += (double)b.x * b.x + (double)b.y * b.y;
-  }
-  const double vv[1] = {acc};
-  const int sl[1] = {SC_RR_RHO + 0};
-  grid_finish<1>(vv, a.partials, a.counter, a.scal_w, sl, red);
-}
-
-// out_rho = M . S (adjoint operator)
-__global__ void __launch_bounds__(kVecThreads) rho_adj_kernel(VecArgs a, int L) {
-  const int n = L / 2, q = L / 4;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.nrho; i += (long long)gridDim.x * blockDim.x) {
-    const int y = (int)(i / L), xx = (int)(i % L);
-    float2 s = make_float2(0.f, 0.f);
-    if (y >= q && y < q + n && xx >= q && xx < q + n) s = a.S[(size_t)(y - q) * n + (xx - q)];
-    a.out[i] = s;
-  }
-}
-
 // CG step: gamma = rr / <p,Ap>; dx += gamma p; r -= gamma Ap; <r,r> (rho, chat partials).
 // Last iteration: x += dx + gamma p (the Newton update x_{n+1} = x_n + dx, Eq. 3).
 __global__ void __launch_bounds__(kVecThreads) cg_update_kernel(VecArgs a) {
   __shared__ double red[32];
   const float gamma = cg_gamma(a.scal, a.iter);
   double acc_rho = 0.0, acc_chat = 0.0;
-  // two complex numbers per thread-iteration (16-byte accesses); ntot is even (N % 16 == 0)
-  const long long n2 = a.ntot / 2;
+  // two complex numbers per 16-byte access; U independent accesses per thread in flight together
+  constexpr int U = 4;
+  const long long n2 = a.ntot / 2, stride = (long long)gridDim.x * blockDim.x;
   const float4* p4 = reinterpret_cast<const float4*>(a.p);
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
-    const float4 pv = p4[i];
-    float4 d = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (a.iter > 0) d = reinterpret_cast<const float4*>(a.dx)[i];
-    d.x = fmaf(gamma, pv.x, d.x); d.y = fmaf(gamma, pv.y, d.y);
-    d.z = fmaf(gamma, pv.z, d.z); d.w = fmaf(gamma, pv.w, d.w);
-    if (a.last) {
-      float4 xv = reinterpret_cast<float4*>(a.x)[i];
-      xv.x += d.x; xv.y += d.y; xv.z += d.z; xv.w += d.w;
-      reinterpret_cast<float4*>(a.x)[i] = xv;
-    } else {
-      reinterpret_cast<float4*>(a.dx)[i] = d;
-      const float4 av = reinterpret_cast<const float4*>(a.Ap)[i];
-      float4 rv = reinterpret_cast<float4*>(a.r)[i];
-      rv.x = fmaf(-gamma, av.x, rv.x); rv.y = fmaf(-gamma, av.y, rv.y);
-      rv.z = fmaf(-gamma, av.z, rv.z); rv.w = fmaf(-gamma, av.w, rv.w);
-      reinterpret_cast<float4*>(a.r)[i] = rv;
-      const double s = (double)rv.x * rv.x + (double)rv.y * rv.y + (double)rv.z * rv.z + (double)rv.w * rv.w;
-      if (2 * i < a.nrho) acc_rho += s; else acc_chat += s;
+  float4* dx4 = reinterpret_cast<float4*>(a.dx);
+  float4* r4 = reinterpret_cast<float4*>(a.r);
+  float4* x4 = reinterpret_cast<float4*>(a.x);
+  const float4* ap4 = reinterpret_cast<const float4*>(a.Ap);
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n2; i0 += U * stride) {
+    float4 pv[U], d[U], w[U], rv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + u * stride;
+      const bool ok = i < n2;
+      pv[u] = ok ? __ldg(p4 + i) : z4;
+      d[u] = (ok && a.iter > 0) ? dx4[i] : z4;
+      if (a.last) {
+        w[u] = ok ? x4[i] : z4;
+      } else {
+        w[u] = ok ? __ldg(ap4 + i) : z4;
+        rv[u] = ok ? r4[i] : z4;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + u * stride;
+      if (i >= n2) continue;
+      float4 dd = d[u];
+      dd.x = fmaf(gamma, pv[u].x, dd.x); dd.y = fmaf(gamma, pv[u].y, dd.y);
+      dd.z = fmaf(gamma, pv[u].z, dd.z); dd.w = fmaf(gamma, pv[u].w, dd.w);
+      if (a.last) {
+        float4 xv = w[u];
+        xv.x += dd.x; xv.y += dd.y; xv.z += dd.z; xv.w += dd.w;
+        x4[i] = xv;
+      } else {
+        dx4[i] = dd;
+        float4 r = rv[u];
+        r.x = fmaf(-gamma, w[u].x, r.x); r.y = fmaf(-gamma, w[u].y, r.y);
+        r.z = fmaf(-gamma, w[u].z, r.z); r.w = fmaf(-gamma, w[u].w, r.w);
+        r4[i] = r;
+        const double sq = (double)r.x * r.x + (double)r.y * r.y + (double)r.z * r.z + (double)r.w * r.w;
+        if (2 * i < a.nrho) acc_rho += sq; else acc_chat += sq;
+      }
     }
   }
   if (!a.last) {
@@ -96,14 +66,31 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_kernel(VecArgs a) {
   }
 }
 
-// frame output: image = crop_Omega(rho) . sqrt(sum_j |c_j|^2)
-__global__ void image_kernel(const float2* __restrict__ rho_omega, const float* __restrict__ rss, float2* img, int Q) {
+// frame output: image = crop_Omega(rho) . sqrt(sum_j |c_j|^2), planes summed in order
+__global__ void image_kernel(const float2* __restrict__ rho_omega, const float* __restrict__ rss, int nplanes,
+                             float2* img, int Q) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Q; i += gridDim.x * blockDim.x) {
-    const float s = sqrtf(rss[i]);
-    img[i] = cscale(rho_omega[i], s);
+    float s = 0.f;
+    for (int j = 0; j < nplanes; ++j) s += rss[(size_t)j * Q + i];
+    img[i] = cscale(rho_omega[i], sqrtf(s));
   }
 }
 
+// local coil sums before the cross-rank all-reduce (world > 1)
+__global__ void coil_sum_kernel(const float2* __restrict__ S_all, int J, float2* S, int Q) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Q; i += gridDim.x * blockDim.x) {
+    float2 s = make_float2(0.f, 0.f);
+    for (int j = 0; j < J; ++j) s = cadd(s, S_all[(size_t)j * Q + i]);
+    S[i] = s;
+  }
+}
+__global__ void rss_sum_kernel(const float* __restrict__ rss_all, int J, float* rss, int Q) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Q; i += gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int j = 0; j < J; ++j) s += rss_all[(size_t)j * Q + i];
+    rss[i] = s;
+  }
+}
 
 bool supported_ng(int ng) {
 #define X(L) if (ng == L) return true;
@@ -142,20 +129,8 @@ static int vec_grid(long long n) {
   return (int)b;
 }
 
-cudaError_t launch_rho_finish(int ng, const VecArgs& a, int with_dot, cudaStream_t s) {
-  rho_finish_kernel<<<vec_grid(a.nrho), kVecThreads, 0, s>>>(a, ng, with_dot);
-  return cudaGetLastError();
-}
-cudaError_t launch_rho_rhs(int ng, const VecArgs& a, cudaStream_t s) {
-  rho_rhs_kernel<<<vec_grid(a.nrho), kVecThreads, 0, s>>>(a, ng);
-  return cudaGetLastError();
-}
-cudaError_t launch_rho_adj(int ng, const VecArgs& a, cudaStream_t s) {
-  rho_adj_kernel<<<vec_grid(a.nrho), kVecThreads, 0, s>>>(a, ng);
-  return cudaGetLastError();
-}
 cudaError_t launch_cg_update(int /*ng*/, const VecArgs& a, cudaStream_t s) {
-  cg_update_kernel<<<vec_grid(a.ntot / 2), kVecThreads, 0, s>>>(a);
+  cg_update_kernel<<<vec_grid((a.ntot / 2 + 3) / 4), kVecThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 __global__ void init_x_kernel(float2* x, long long nrho, long long ntot) {
@@ -174,10 +149,32 @@ int col_tiles(int ng) {
   return 0;
 }
 
-cudaError_t launch_image(int ng, const float2* rho_omega, const float* rss, float2* img, cudaStream_t s) {
+cudaError_t launch_image(int ng, const float2* rho_omega, const float* rss, int nplanes, float2* img, cudaStream_t s) {
   const int Q = (ng / 2) * (ng / 2);
-  image_kernel<<<(Q + 255) / 256, 256, 0, s>>>(rho_omega, rss, img, Q);
+  image_kernel<<<(Q + 255) / 256, 256, 0, s>>>(rho_omega, rss, nplanes, img, Q);
   return cudaGetLastError();
+}
+cudaError_t launch_coil_sum(int ng, const float2* S_all, int J, float2* S, cudaStream_t s) {
+  const int Q = (ng / 2) * (ng / 2);
+  coil_sum_kernel<<<(Q + 255) / 256, 256, 0, s>>>(S_all, J, S, Q);
+  return cudaGetLastError();
+}
+cudaError_t launch_rss_sum(int ng, const float* rss_all, int J, float* rss, cudaStream_t s) {
+  const int Q = (ng / 2) * (ng / 2);
+  rss_sum_kernel<<<(Q + 255) / 256, 256, 0, s>>>(rss_all, J, rss, Q);
+  return cudaGetLastError();
+}
+cudaError_t launch_frame(int ng, const FrameArgs& f, cudaStream_t s) {
+#define X(L) if (ng == L) return launch_frame_##L(f, s);
+  NLV_FOR_EACH_NG(X)
+#undef X
+  return cudaErrorInvalidValue;
+}
+bool frame_supported(int ng) {
+#define X(L) if (ng == L) return frame_ok_##L();
+  NLV_FOR_EACH_NG(X)
+#undef X
+  return false;
 }
 
 }  // namespace nlv

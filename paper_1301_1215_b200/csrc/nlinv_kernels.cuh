@@ -59,6 +59,13 @@ struct ColArgs {
   double* partials;        // reduction partials for this launch
   unsigned* counter;
   int out_slot;            // scalar index the finished reduction is written to (-1: none)
+  int out_slot_rho;        // scalar index of the rho-block partial (FFT_W modes)
+  float beta;              // CG beta for CK_IFFT_W_CG (set by the launcher / frame kernel)
+  int nS;                  // number of [n][n] planes of S summed (in order) by the rho slice
+  const float2* S;         // coil-sum planes [nS][n][n] (rho slice of the FFT_W modes)
+  const float2* rho_a;     // rho-slice operand (p_rho for NORMAL, rho for RHS)
+  const float2* rho_b;     // rho_ref for RHS
+  float2* rho_out;         // rho-slice output (Ap_rho / adjoint rho)
   int iter;                // CG iteration (beta for CK_IFFT_W_CG)
   float alpha;
   int J;
@@ -71,10 +78,26 @@ struct RowArgs {
   float2* rho_omega;       // [n][n]
   const float2* xrho;      // rho of the point, full grid (set point)
   const float2* prho;      // rho part of the direction, full grid (K2)
-  float2* S;               // [n][n] coil-sum partial (K4)
-  float* rss;              // [n][n] sum |c_j|^2 (RSS)
+  float2* S;               // [J][n][n] per-coil terms conj(c_j) u_j (K4)
+  float* rss;              // [J][n][n] per-coil |c_j|^2 (RSS)
   int J;
-  int gc;                  // coil groups per CTA
+};
+
+// Persistent whole-frame kernel (world == 1): every buffer of the plan.
+constexpr int kMaxFrameBlocks = 1024;
+struct FrameArgs {
+  float2 *x, *xref, *dx, *r, *p, *Ap, *tA, *tB, *c_omega, *rho_omega, *S_all, *img;
+  float* rss_all;
+  const float2* y;
+  const float* winv;
+  const uint8_t* mask;
+  const float2* tw;
+  double* scal;
+  double* red;             // [3][2 * kMaxFrameBlocks] reduction partials
+  unsigned* bar_count;
+  unsigned* bar_gen;
+  int J, K, L;
+  double alpha0, q;
 };
 
 struct VecArgs {
@@ -100,15 +123,16 @@ struct VecArgs {
 // launchers (return cudaGetLastError())
 cudaError_t launch_col(int ng, int mode, const ColArgs& a, const float2* tw, cudaStream_t s);
 cudaError_t launch_row(int ng, int mode, const RowArgs& a, const float2* tw, cudaStream_t s);
-cudaError_t launch_rho_finish(int ng, const VecArgs& a, int with_dot, cudaStream_t s);
-cudaError_t launch_rho_rhs(int ng, const VecArgs& a, cudaStream_t s);
-cudaError_t launch_rho_adj(int ng, const VecArgs& a, cudaStream_t s);
 cudaError_t launch_cg_update(int ng, const VecArgs& a, cudaStream_t s);
-cudaError_t launch_image(int ng, const float2* rho_omega, const float* rss, float2* img, cudaStream_t s);
+cudaError_t launch_image(int ng, const float2* rho_omega, const float* rss, int nplanes, float2* img, cudaStream_t s);
 cudaError_t launch_fft2d(int ng, const float2* in, float2* out, int batch, int inverse, const float2* tw,
                          float2* tmp, cudaStream_t s);
 bool supported_ng(int ng);
 int col_tiles(int ng);  // column-kernel CTAs per coil
 cudaError_t launch_init_x(float2* x, long long nrho, long long ntot, cudaStream_t s);
+cudaError_t launch_frame(int ng, const FrameArgs& f, cudaStream_t s);
+bool frame_supported(int ng);
+cudaError_t launch_coil_sum(int ng, const float2* S_all, int J, float2* S, cudaStream_t s);
+cudaError_t launch_rss_sum(int ng, const float* rss_all, int J, float* rss, cudaStream_t s);
 
 }  // namespace nlv

@@ -66,6 +66,10 @@ _SIGS = {
     "nlinv_plan_stats": (c_int, [c_void_p, ctypes.POINTER(Stats)]),
     "nlinv_debug_fft2d": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]),
     "nlinv_plan_launch_count": (c_ll, [c_void_p]),
+    "nlinv_stream_frame": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]),
+    "nlinv_stream_reset": (c_int, [c_void_p]),
+    "nlinv_plan_set_profiling": (c_int, [c_void_p, c_int]),
+    "nlinv_plan_profile_json": (c_int, [c_void_p, ctypes.c_char_p, ctypes.c_size_t]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -231,6 +235,39 @@ class Plan:
                                            host(image_out, self.image_shape, "image_out"),
                                            _stream_ptr(stream)), self._h)
         return x_out, image_out
+
+    def stream_frame(self, frame, mask=None, newton_steps=7, cg_iters=10, image_out=None, stream=None):
+        """Real-time entry: host complex64 frame (pinned), optional host uint8 mask, host image out."""
+        import torch
+        if frame.is_cuda or frame.dtype != torch.complex64 or tuple(frame.shape) != self.y_shape \
+                or not frame.is_contiguous():
+            raise ValueError(f"frame must be a contiguous CPU complex64 tensor of shape {self.y_shape}")
+        mp = None
+        if mask is not None:
+            if not (isinstance(mask, torch.Tensor) and not mask.is_cuda and mask.dtype == torch.uint8
+                    and tuple(mask.shape) == (self.ng, self.ng) and mask.is_contiguous()):
+                raise ValueError("mask must be a contiguous CPU uint8 tensor [ng, ng]")
+            mp = ctypes.c_void_p(mask.data_ptr())
+        ip = None
+        if image_out is not None:
+            if image_out.is_cuda or image_out.dtype != torch.complex64 or tuple(image_out.shape) != self.image_shape:
+                raise ValueError("image_out must be a CPU complex64 tensor [n, n]")
+            ip = ctypes.c_void_p(image_out.data_ptr())
+        _check(_lib.nlinv_stream_frame(self._h, ctypes.c_void_p(frame.data_ptr()), mp, int(newton_steps),
+                                       int(cg_iters), ip, _stream_ptr(stream)), self._h)
+        return image_out
+
+    def stream_reset(self):
+        _check(_lib.nlinv_stream_reset(self._h), self._h)
+
+    def set_profiling(self, on: bool):
+        _check(_lib.nlinv_plan_set_profiling(self._h, int(bool(on))), self._h)
+
+    def profile(self) -> dict:
+        import json
+        buf = ctypes.create_string_buffer(1 << 16)
+        _check(_lib.nlinv_plan_profile_json(self._h, buf, len(buf)), self._h)
+        return {k: {"launches": v[0], "ms": v[1]} for k, v in json.loads(buf.value.decode()).items()}
 
     def stats(self):
         s = Stats()
