@@ -92,7 +92,7 @@ class Clocks:
         self.p = None
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                       "-lms", "100", "-i", str(device)], stdout=subprocess.PIPE,
+                                       "-lms", "50", "-i", str(device)], stdout=subprocess.PIPE,
                                       stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.p = None
@@ -135,17 +135,14 @@ def make_frames(rank_first: int, count: int):
 def run_ours(args):
     import torch
     import torch.distributed as dist
-    from paper_1301_1215_b200 import Plan, get_unique_id
+    from paper_1301_1215_b200 import Plan
 
     world, rank, local = _dist()
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        obj = [get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
-    else:
-        nccl_id = None
+    from paper_1301_1215_b200.dist import exchange_unique_id
+    nccl_id = exchange_unique_id(rank, world)
 
     from paper_1301_1215_b200 import radial_mask
     mask0 = radial_mask(NG, SPOKES, TURNS, 0)

@@ -183,6 +183,11 @@ nlinv_status nlinv_stream_reset(nlinv_plan plan);
 nlinv_status nlinv_plan_set_profiling(nlinv_plan plan, int on);
 nlinv_status nlinv_plan_profile_json(nlinv_plan plan, char* buf, size_t len);
 
+/* Diagnostics of the persistent frame kernel: enable != 0 allocates/clears a timestamp buffer
+ * (CTA 0 records %globaltimer after every grid barrier of later frames); enable == 0 copies up
+ * to cap timestamps (ns) into out and their number into *count. */
+nlinv_status nlinv_plan_phase_times(nlinv_plan plan, int enable, unsigned long long* out, int cap, int* count);
+
 /* Statistics of the last reconstruct (synchronises the plan's last stream). */
 nlinv_status nlinv_plan_stats(nlinv_plan plan, nlinv_stats* out);
 

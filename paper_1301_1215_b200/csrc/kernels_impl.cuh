@@ -672,6 +672,16 @@ __device__ __forceinline__ void row_phase(const RowArgs& a, const float2* tw, fl
   }
 }
 
+// optional phase timestamps (CTA 0, after each barrier) for the per-phase breakdown
+__device__ __forceinline__ void stamp(const FrameArgs& f, int& ns) {
+  if (f.tstamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && ns < f.tstamp_cap) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    f.tstamp[ns] = t;
+  }
+  ++ns;
+}
+
 template <int L>
 __global__ void __launch_bounds__(256, 2) frame_kernel(FrameArgs f) {
   constexpr int n = L / 2, q = L / 4;
@@ -682,6 +692,8 @@ __global__ void __launch_bounds__(256, 2) frame_kernel(FrameArgs f) {
   double* sred = reinterpret_cast<double*>(reinterpret_cast<char*>(xb) + FrameGeo<L>::XB);
   for (int i = threadIdx.x; i < L; i += blockDim.x) tw[i] = f.tw[i];
   __syncthreads();
+  int nstamp = 0;
+  stamp(f, nstamp);
 
   const int J = f.J;
   ColArgs ca{};
@@ -707,24 +719,28 @@ __global__ void __launch_bounds__(256, 2) frame_kernel(FrameArgs f) {
     ca.out = f.tA;
     col_phase<L, CK_IFFT_W>(ca, tw, xb, J, d0, d1);
     grid_barrier(f.bar_count, f.bar_gen);
+    stamp(f, nstamp);
     // N2: row half of c_j, c|Omega, rho|Omega, and the row FFT of rho c_j (forward operator)
     ra.in = f.tA;
     ra.out = f.tB;
     ra.xrho = f.x;
     row_phase<L, RK_SETPOINT_FWD>(ra, tw, xb);
     grid_barrier(f.bar_count, f.bar_gen);
+    stamp(f, nstamp);
     // N3: column FFT -> r = P (y - F x) (+ ||r||^2) -> column IFFT (adjoint head)
     ca.in = f.tB;
     ca.out = f.tA;
     d0 = d1 = 0.0;
     col_phase<L, CK_RESADJ>(ca, tw, xb, J, d0, d1);
     double2 res = grid_reduce2(d0, d1, f.red + 0 * 2 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
+    stamp(f, nstamp);
     if (blockIdx.x == 0 && threadIdx.x == 0) f.scal[SC_RES + nstep] = res.y;
     // N4: row IFFT -> u, per-coil conj(c) u, conj(rho) u -> row FFT
     ra.in = f.tA;
     ra.out = f.tB;
     row_phase<L, RK_K4>(ra, tw, xb);
     grid_barrier(f.bar_count, f.bar_gen);
+    stamp(f, nstamp);
     // N5: rhs b = DF^H r - alpha (x - x_ref); r = p = b
     ca.in = f.tB;
     ca.src = f.x + N;
@@ -739,6 +755,7 @@ __global__ void __launch_bounds__(256, 2) frame_kernel(FrameArgs f) {
     d0 = d1 = 0.0;
     col_phase<L, CK_FFT_W_RHS>(ca, tw, xb, J + 1, d0, d1);
     double2 rr2 = grid_reduce2(d0, d1, f.red + 1 * 2 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
+    stamp(f, nstamp);
     double rr = rr2.x + rr2.y, rr_prev = rr;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       f.scal[SC_RR_RHO] = rr2.x;
@@ -755,22 +772,26 @@ __global__ void __launch_bounds__(256, 2) frame_kernel(FrameArgs f) {
       ca.beta = (it == 0 || rr_prev == 0.0) ? 0.0f : (float)(rr / rr_prev);
       col_phase<L, CK_IFFT_W_CG>(ca, tw, xb, J + 1, d0, d1);
       grid_barrier(f.bar_count, f.bar_gen);
+      stamp(f, nstamp);
       // P2: K2
       ra.in = f.tA;
       ra.out = f.tB;
       ra.prho = f.p;
       row_phase<L, RK_K2>(ra, tw, xb);
       grid_barrier(f.bar_count, f.bar_gen);
+      stamp(f, nstamp);
       // P3: K3 (PSF convolution)
       ca.in = f.tB;
       ca.out = f.tA;
       col_phase<L, CK_PSF>(ca, tw, xb, J, d0, d1);
       grid_barrier(f.bar_count, f.bar_gen);
+      stamp(f, nstamp);
       // P4: K4
       ra.in = f.tA;
       ra.out = f.tB;
       row_phase<L, RK_K4>(ra, tw, xb);
       grid_barrier(f.bar_count, f.bar_gen);
+      stamp(f, nstamp);
       // P5: K5 + rho slice: Ap, <p, Ap>
       ca.in = f.tB;
       ca.src2 = f.p + N;
@@ -781,6 +802,7 @@ __global__ void __launch_bounds__(256, 2) frame_kernel(FrameArgs f) {
       d0 = d1 = 0.0;
       col_phase<L, CK_FFT_W_NORMAL>(ca, tw, xb, J + 1, d0, d1);
       double2 pap = grid_reduce2(d0, d1, f.red + 2 * 2 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
+      stamp(f, nstamp);
       const double papt = pap.x + pap.y;
       const float gamma = (rr != 0.0) ? (float)(rr / papt) : 0.0f;
       if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -819,6 +841,7 @@ __global__ void __launch_bounds__(256, 2) frame_kernel(FrameArgs f) {
       }
       if (!last) {
         double2 r2 = grid_reduce2(ar, ac, f.red + 1 * 2 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
+        stamp(f, nstamp);
         rr_prev = rr;
         rr = r2.x + r2.y;
         if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -827,6 +850,7 @@ __global__ void __launch_bounds__(256, 2) frame_kernel(FrameArgs f) {
         }
       } else {
         grid_barrier(f.bar_count, f.bar_gen);
+        stamp(f, nstamp);
       }
     }
   }
@@ -836,10 +860,12 @@ __global__ void __launch_bounds__(256, 2) frame_kernel(FrameArgs f) {
     ca.out = f.tA;
     col_phase<L, CK_IFFT_W>(ca, tw, xb, J, d0, d1);
     grid_barrier(f.bar_count, f.bar_gen);
+    stamp(f, nstamp);
     ra.in = f.tA;
     ra.xrho = f.x;
     row_phase<L, RK_RSS>(ra, tw, xb);
     grid_barrier(f.bar_count, f.bar_gen);
+    stamp(f, nstamp);
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)Q;
          i += (long long)gridDim.x * blockDim.x) {
       float s = 0.f;

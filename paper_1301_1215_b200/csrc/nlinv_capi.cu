@@ -61,6 +61,8 @@ struct nlinv_plan_s {
   double* fred = nullptr;        // frame-kernel reduction partials
   unsigned* fbar = nullptr;      // frame-kernel grid barrier (count, generation)
   bool use_frame = false;
+  bool gexec_valid_reset = false;
+  unsigned long long* tstamp = nullptr;   // frame-kernel phase timestamps (nlinv_plan_phase_times)
   double *scal = nullptr, *partials = nullptr;
   unsigned* counter = nullptr;
   // host e2e staging (device side)
@@ -222,7 +224,7 @@ static void plan_free(nlinv_plan pl) {
   if (!pl) return;
   void* ptrs[] = {pl->tw, pl->winv, pl->mask, pl->xref, pl->dx, pl->r, pl->p, pl->Ap, pl->tA, pl->tB,
                   pl->c_omega, pl->rho_omega, pl->S_all, pl->S, pl->S_sum, pl->rss_all, pl->rss, pl->rss_sum,
-                  pl->fred, pl->fbar, pl->scal, pl->partials,
+                  pl->fred, pl->fbar, pl->tstamp, pl->scal, pl->partials,
                   pl->counter, pl->h_frame, pl->h_x, pl->h_img};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -596,6 +598,8 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
     f.L = L;
     f.alpha0 = pl->prm.alpha0;
     f.q = pl->prm.q;
+    f.tstamp = pl->tstamp;
+    f.tstamp_cap = pl->tstamp ? 8192 : 0;
     return q.kern("frame", [&] { return launch_frame(pl->ng, f, q.s); });
   }
   double alpha_d = pl->prm.alpha0;
@@ -774,6 +778,11 @@ extern "C" nlinv_status nlinv_reconstruct(nlinv_plan pl, const nlinv_c32* frame,
   key.L = cg_iters;
   key.stream = s;
   const bool use_graph = (s != nullptr) && !pl->prof && (std::getenv("NLINV_NO_GRAPH") == nullptr);
+  if (pl->gexec_valid_reset && pl->gexec) {
+    cudaGraphExecDestroy(pl->gexec);
+    pl->gexec = nullptr;
+    pl->gexec_valid_reset = false;
+  }
   if (use_graph && pl->gexec && pl->gkey == key) {
     CU(cudaGraphLaunch(pl->gexec, s));
     pl->launches += pl->gkernels;
@@ -924,5 +933,25 @@ extern "C" nlinv_status nlinv_plan_profile_json(nlinv_plan pl, char* buf, size_t
   pl->ev_used = 0;
   if (out.size() + 1 > len) return fail(pl, NLINV_ERR_SIZE, "profile buffer too small");
   std::memcpy(buf, out.c_str(), out.size() + 1);
+  return NLINV_OK;
+}
+
+// ------------------------------------------------------------------ frame-kernel phase timestamps
+extern "C" nlinv_status nlinv_plan_phase_times(nlinv_plan pl, int enable, unsigned long long* out, int cap,
+                                               int* count) {
+  if (!pl) return fail(pl, NLINV_ERR_ARG, "NULL plan");
+  if (enable) {
+    if (!pl->tstamp) CU(cudaMalloc((void**)&pl->tstamp, sizeof(unsigned long long) * 8192));
+    CU(cudaMemset(pl->tstamp, 0, sizeof(unsigned long long) * 8192));
+    pl->gexec_valid_reset = true;
+    return NLINV_OK;
+  }
+  if (!pl->tstamp || !out || !count) return fail(pl, NLINV_ERR_STATE, "phase timing not enabled");
+  CU(cudaDeviceSynchronize());
+  const int n = cap < 8192 ? cap : 8192;
+  CU(cudaMemcpy(out, pl->tstamp, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost));
+  int c = 0;
+  while (c < n && out[c] != 0) ++c;
+  *count = c;
   return NLINV_OK;
 }

@@ -98,6 +98,8 @@ struct FrameArgs {
   unsigned* bar_gen;
   int J, K, L;
   double alpha0, q;
+  unsigned long long* tstamp;  // optional per-phase timestamps (ns), CTA 0
+  int tstamp_cap;
 };
 
 struct VecArgs {
