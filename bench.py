@@ -46,15 +46,18 @@ def _peaks():
 
 
 # Algorithmic (compulsory) bytes per launch, each operand read once and each result written once
-# at its minimal support. N = ng^2, Jl = local coils, c64 = 8 B.
-def algo_bytes(name: str, ng: int, Jl: int, it: int = 1, L: int = CG) -> float:
+# at its minimal support (DESIGN.md §7 Roofline). N = ng^2, Jl = local coils, c64 = 8 B.
+def algo_bytes(name: str, ng: int, Jl: int, L: int = CG) -> float:
     N = ng * ng
     t = {
-        "col_ifft_w_cg": 28 * Jl * N + 4 * N + 24 * N,
+        # K1: r, p, dx in; p, dx, T1 out per coil (+ rho slice, w^-1); dx skipped at iterations 0-1
+        "col_ifft_w_cg": (8 + 8 + 8 + 8 + 8 + 4) * Jl * N + 4 * N + 40 * N,
         "row_k2": 10 * Jl * N + 4 * N,
         "col_psf": 8 * Jl * N + N,
         "row_k4": 10 * Jl * N + 4 * N,
         "col_fft_w_normal": 20 * Jl * N + 4 * N + 18 * N,   # + rho slice: S, p_rho in, Ap_rho out
+        "r_update": 24 * N * (Jl + 1),                       # r, Ap in; r out
+        "newton_update": 32 * N * (Jl + 1),                  # p, dx, x in; x out
         "col_ifft_w": 8 * Jl * N + 4 * N + 4 * Jl * N,
         "row_setpoint_fwd": 4 * Jl * N + 2 * Jl * N + 4 * Jl * N + 2 * N + 2 * N,
         "row_setpoint": 4 * Jl * N + 2 * Jl * N + 4 * N,
@@ -65,20 +68,14 @@ def algo_bytes(name: str, ng: int, Jl: int, it: int = 1, L: int = CG) -> float:
         "image": 2 * N + N + 2 * N,
     }
     if name == "frame":
-        # the persistent whole-frame kernel: every pass of the multi-kernel path, same bytes
-        K = NEWTON
+        # the persistent whole-frame kernel (NLINV_FRAME=1): every pass of the multi-kernel path
         newton = sum(algo_bytes(k, ng, Jl) for k in ("col_ifft_w", "row_setpoint_fwd", "col_resadj", "row_k4",
-                                                    "col_fft_w_rhs"))
-        cg = sum(algo_bytes(k, ng, Jl) for k in ("col_ifft_w_cg", "row_k2", "col_psf", "row_k4",
-                                                "col_fft_w_normal"))
-        upd = algo_bytes("cg_update", ng, Jl) * L
+                                                    "col_fft_w_rhs", "newton_update"))
+        cgp = sum(algo_bytes(k, ng, Jl) for k in ("col_ifft_w_cg", "row_k2", "col_psf", "row_k4",
+                                                 "col_fft_w_normal"))
+        upd = algo_bytes("r_update", ng, Jl) * (L - 1)
         out = algo_bytes("col_ifft_w", ng, Jl) + algo_bytes("row_rss", ng, Jl) + algo_bytes("image", ng, Jl)
-        return K * (newton + L * cg + upd) + out
-    if name == "cg_update":
-        nb = Jl + 1
-        # iteration 0 skips the dx read; the last iteration only reads p, dx, x and writes x
-        per = [(40 if i == 0 else 48) if i < L - 1 else (24 if i == 0 else 32) for i in range(L)]
-        return statistics.mean(per) * N * nb
+        return NEWTON * (newton + L * cgp + upd) + out
     return float(t.get(name, 0.0))
 
 
@@ -230,10 +227,7 @@ def run_ours(args):
     frame_ms = sum(v["ms"] for v in prof.values())
     top = max(prof.items(), key=lambda kv: kv[1]["ms"])
     tname, tv = top
-    if tname == "cg_update":
-        tb = algo_bytes(tname, NG, plan.count) * tv["launches"]
-    else:
-        tb = algo_bytes(tname, NG, plan.count) * tv["launches"]
+    tb = algo_bytes(tname, NG, plan.count) * tv["launches"]
     achieved = tb / (tv["ms"] / 1e3) / 1e9
     traffic = None
     try:

@@ -188,6 +188,11 @@ nlinv_status nlinv_plan_profile_json(nlinv_plan plan, char* buf, size_t len);
  * to cap timestamps (ns) into out and their number into *count. */
 nlinv_status nlinv_plan_phase_times(nlinv_plan plan, int enable, unsigned long long* out, int cap, int* count);
 
+/* Debug (builds with -DNLV_TRACE only record data): col_mode >= 0 starts recording per-CTA
+ * %globaltimer timelines (8 stamps per CTA) of the column pass with that internal mode;
+ * col_mode < 0 copies up to cap stamps into out and stops recording. */
+nlinv_status nlinv_plan_trace(nlinv_plan plan, int col_mode, unsigned long long* out, int cap);
+
 /* Statistics of the last reconstruct (synchronises the plan's last stream). */
 nlinv_status nlinv_plan_stats(nlinv_plan plan, nlinv_stats* out);
 

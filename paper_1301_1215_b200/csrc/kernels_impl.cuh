@@ -116,16 +116,42 @@ __device__ __forceinline__ void grid_finish(const double (&v)[NV], double* parti
   }
 }
 
-__device__ __forceinline__ float cg_beta(const double* scal, int i) {
-  if (i <= 0) return 0.0f;
-  const double rr = scal[SC_RR_RHO + i] + scal[SC_RR_CHAT + i];
-  const double rp = scal[SC_RR_RHO + i - 1] + scal[SC_RR_CHAT + i - 1];
-  return rp != 0.0 ? (float)(rr / rp) : 0.0f;
-}
+// Textbook CG scalars (R9): gamma_i = rr_i / <p_i, A p_i>, beta_i = rr_{i+1} / rr_i.
+// rr_i and <p_i, A p_i> are published as (rho, chat) parts; rho is replicated and counted once.
+__device__ __forceinline__ double cg_rr(const double* scal, int i) { return scal[SC_RR_RHO + i] + scal[SC_RR_CHAT + i]; }
 __device__ __forceinline__ float cg_gamma(const double* scal, int i) {
-  const double rr = scal[SC_RR_RHO + i] + scal[SC_RR_CHAT + i];
+  const double rr = cg_rr(scal, i);
   const double pap = scal[SC_PAP_RHO + i] + scal[SC_PAP_CHAT + i];
   return rr != 0.0 ? (float)(rr / pap) : 0.0f;
+}
+__device__ __forceinline__ float cg_beta(const double* scal, int i) {  // beta_i
+  const double rr = cg_rr(scal, i);
+  return rr != 0.0 ? (float)(cg_rr(scal, i + 1) / rr) : 0.0f;
+}
+
+// Twiddle table global -> shared with cp.async, so its latency overlaps the pass's own loads;
+// the pass waits for it (tw_wait) right before its first transform.
+__device__ __forceinline__ void tw_copy_async(float2* tw_s, const float2* tw_g, int L) {
+  for (int i = threadIdx.x; i < L; i += blockDim.x) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(tw_s + i);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(tw_g + i));
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+__device__ __forceinline__ void tw_wait() {
+  asm volatile("cp.async.wait_all;\n" ::);
+  __syncthreads();
+}
+
+// debug timeline of one CTA (globaltimer ns), compiled in with -DNLV_TRACE
+__device__ __forceinline__ void trace_stamp(unsigned long long* tr, int k) {
+#ifdef NLV_TRACE
+  if (tr != nullptr && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[(size_t)(blockIdx.y * gridDim.x + blockIdx.x) * 8 + k] = t;
+  }
+#endif
 }
 
 // ------------------------------------------------------------------ column task (one tile of CW columns)
@@ -134,7 +160,8 @@ __device__ __forceinline__ float cg_gamma(const double* scal, int i) {
 // of the CTA must call it (the transform uses __syncthreads).
 template <int L, int MODE>
 __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, const float2* tw, float2* xb,
-                                         double& acc_rho, double& acc) {
+                                         double& acc_rho, double& acc, double* acc3, int rlo = 0, int rhi = L,
+                                         bool tw_async = false) {
   using C = Cfg<L>;
   using S = Sched<L>;
   constexpr int T = C::T, E = C::E, CW = ColGeo<L>::CW;
@@ -147,12 +174,17 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
   const int x = tile * CW + c;
 
   if constexpr (MODE == CK_IFFT_W_CG) {
-    if (j == a.J) {  // rho-block slice of the fused CG direction update p = r + beta p
-      for (int y = t; y < L; y += T) {
+    if (j == a.J) {  // rho-block slice of the fused CG step (same update as the coil tiles below)
+      for (int y = rlo + t; y < rhi; y += T) {
         const size_t i = (size_t)y * L + x;
         const float2 rv = a.rho_r[i], pv = a.rho_p[i];
+        if (a.iter > 0) {
+          const float2 dv = (a.iter > 1) ? a.rho_dx[i] : make_float2(0.f, 0.f);
+          a.rho_dx[i] = make_float2(fmaf(a.gamma, pv.x, dv.x), fmaf(a.gamma, pv.y, dv.y));
+        }
         a.rho_p[i] = make_float2(fmaf(a.beta, pv.x, rv.x), fmaf(a.beta, pv.y, rv.y));
       }
+      if (tw_async) asm volatile("cp.async.wait_all;\n" ::);
       return;
     }
   }
@@ -160,7 +192,7 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
     if (j == a.J) {
       // rho-block slice (replicated rho): out_rho = M . sum_s S_s (+ alpha p_rho | - alpha (rho - rho_ref))
       const bool xin = (x >= q && x < q + n);
-      for (int y = t; y < L; y += T) {
+      for (int y = rlo + t; y < rhi; y += T) {
         const size_t i = (size_t)y * L + x;
         float2 sv = make_float2(0.f, 0.f);
         if (xin && y >= q && y < q + n) {
@@ -182,6 +214,7 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
           a.rho_out[i] = sv;
         }
       }
+      if (tw_async) asm volatile("cp.async.wait_all;\n" ::);
       return;
     }
   }
@@ -190,33 +223,45 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
   float2 v[E];
 
   // ---------------- prologue: pass-0 input pattern, index = row
-  if constexpr (MODE == CK_IFFT_W || MODE == CK_IFFT_W_CG) {
+  if constexpr (MODE == CK_IFFT_W) {
     constexpr int CH = 8;
 #pragma unroll
     for (int e0 = 0; e0 < E; e0 += CH) {
       float wv[CH];
-      float2 rv[CH], pv[CH];
+      float2 rv[CH];
 #pragma unroll
       for (int u = 0; u < CH; ++u) {
         const size_t i = (size_t)S::in_idx(t, e0 + u) * L + x;
         wv[u] = a.winv[i];
-        if constexpr (MODE == CK_IFFT_W_CG) {
-          rv[u] = a.r[j * N + i];
-          pv[u] = a.p[j * N + i];
-        } else {
-          rv[u] = a.src[j * N + i];
-        }
+        rv[u] = a.src[j * N + i];
+      }
+#pragma unroll
+      for (int u = 0; u < CH; ++u) v[e0 + u] = cscale(rv[u], wv[u] * sgn_of(S::in_idx(t, e0 + u)));
+    }
+  } else if constexpr (MODE == CK_IFFT_W_CG) {
+    // fused CG step: dx += gamma_{i-1} p_{i-1}; p_i = r_i + beta_{i-1} p_{i-1} (iteration 0: p = r)
+    constexpr int CH = 8;
+    const bool upd = a.iter > 0, hasdx = a.iter > 1;
+#pragma unroll
+    for (int e0 = 0; e0 < E; e0 += CH) {
+      float wv[CH];
+      float2 rv[CH], pv[CH], dv[CH];
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const size_t i = j * N + (size_t)S::in_idx(t, e0 + u) * L + x;
+        wv[u] = a.winv[(size_t)S::in_idx(t, e0 + u) * L + x];
+        rv[u] = a.r[i];
+        pv[u] = a.p[i];
+        dv[u] = hasdx ? a.dx[i] : make_float2(0.f, 0.f);
       }
 #pragma unroll
       for (int u = 0; u < CH; ++u) {
         const int yr = S::in_idx(t, e0 + u);
-        const size_t i = (size_t)yr * L + x;
-        float2 s = rv[u];
-        if constexpr (MODE == CK_IFFT_W_CG) {
-          s = make_float2(fmaf(a.beta, pv[u].x, rv[u].x), fmaf(a.beta, pv[u].y, rv[u].y));
-          a.p[j * N + i] = s;
-        }
-        v[e0 + u] = cscale(s, wv[u] * sgn_of(yr));
+        const size_t i = j * N + (size_t)yr * L + x;
+        if (upd) a.dx[i] = make_float2(fmaf(a.gamma, pv[u].x, dv[u].x), fmaf(a.gamma, pv[u].y, dv[u].y));
+        const float2 sv = make_float2(fmaf(a.beta, pv[u].x, rv[u].x), fmaf(a.beta, pv[u].y, rv[u].y));
+        a.p[i] = sv;
+        v[e0 + u] = cscale(sv, wv[u] * sgn_of(yr));
       }
     }
   } else if constexpr (MODE == CK_ADJ1) {
@@ -246,7 +291,10 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
     for (int e = 0; e < E; ++e) mbits |= (a.mask[(size_t)S::out_idx(t, e) * L + x] ? 1u : 0u) << e;
   }
 
+  if (tw_async) tw_wait();
+  trace_stamp(a.trace, 1);
   fft<L, DIR_FIRST>(v, t, tw, buf, SyncBlock{});
+  trace_stamp(a.trace, 2);
 
   // ---------------- middle: k-space pointwise (registers hold output pattern, index = k)
   if constexpr (MODE == CK_PSF || MODE == CK_RESADJ) {
@@ -269,7 +317,9 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
       }
     }
     out_to_in<L>(v, t, buf, SyncBlock{});
+    trace_stamp(a.trace, 3);
     fft<L, +1>(v, t, tw, buf, SyncBlock{});
+    trace_stamp(a.trace, 4);
   }
 
   // ---------------- epilogue: last-pass output pattern, index = row k
@@ -329,34 +379,44 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
 }
 
 template <int L, int MODE>
-__global__ void __launch_bounds__(ColGeo<L>::THREADS) col_kernel(ColArgs a, const float2* __restrict__ twg) {
+#ifndef NLV_MINB
+#define NLV_MINB 2  // <= 128 registers: two 256-thread CTAs per SM (more registers halve residency)
+#endif
+__global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColArgs a, const float2* __restrict__ twg) {
   constexpr int CW = ColGeo<L>::CW, NT = ColGeo<L>::THREADS;
   extern __shared__ float4 smem_raw[];
   float2* tw = reinterpret_cast<float2*>(smem_raw);
   float2* xb = tw + L;
   double* red = reinterpret_cast<double*>(xb + (size_t)L * CW);
-  for (int i = threadIdx.x; i < L; i += NT) tw[i] = twg[i];
-  __syncthreads();
-  if constexpr (MODE == CK_IFFT_W_CG) a.beta = cg_beta(a.scal, a.iter);
+  trace_stamp(a.trace, 0);
+  tw_copy_async(tw, twg, L);
+  if constexpr (MODE == CK_IFFT_W_CG) {
+    a.gamma = (a.iter > 0) ? cg_gamma(a.scal, a.iter - 1) : 0.0f;
+    a.beta = (a.iter > 0) ? cg_beta(a.scal, a.iter - 1) : 0.0f;
+  }
   double acc_rho = 0.0, acc = 0.0;
   // the rho slice (when present) is blockIdx.y == 0 so it is scheduled first
   const bool has_rho = (MODE == CK_IFFT_W_CG || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ);
   const int j = has_rho ? (blockIdx.y == 0 ? a.J : (int)blockIdx.y - 1) : (int)blockIdx.y;
-  col_task<L, MODE>(a, blockIdx.x, j, tw, xb, acc_rho, acc);
-  if constexpr (MODE == CK_RESADJ || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS) {
+  double acc3[4] = {0.0, 0.0, 0.0, 0.0};
+  col_task<L, MODE>(a, blockIdx.x, j, tw, xb, acc_rho, acc, acc3, 0, L, true);
+  trace_stamp(a.trace, 5);
+  if constexpr (MODE == CK_RESADJ || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_NORMAL) {
     if (a.partials != nullptr) {
       const double vv[2] = {acc_rho, acc};
       const int sl[2] = {a.out_slot_rho, a.out_slot};
       grid_finish<2>(vv, a.partials, a.counter, a.scal_w, sl, red);
     }
   }
+  trace_stamp(a.trace, 6);
 }
 
 // ------------------------------------------------------------------ row task (one (coil, Omega row) per group)
 // Group g of the CTA (T threads) handles pair pair0 + g, pairs ordered coil-major (j * n + yy).
 // Groups are independent (each inside one warp); no CTA-wide barrier is used.
 template <int L, int MODE>
-__device__ __forceinline__ void row_task(const RowArgs& a, int pair0, const float2* tw, float2* xbase) {
+__device__ __forceinline__ void row_task(const RowArgs& a, int pair0, const float2* tw, float2* xbase,
+                                         bool tw_async = false) {
   using C = Cfg<L>;
   using S = Sched<L>;
   constexpr int T = C::T, E = C::E;
@@ -381,6 +441,7 @@ __device__ __forceinline__ void row_task(const RowArgs& a, int pair0, const floa
     v[e] = make_float2(0.f, 0.f);
     if (active) v[e] = cneg_if(a.in[j * H + (size_t)yy * L + xi], xi & 1);
   }
+  if (tw_async) tw_wait();
   fft<L, +1>(v, t, tw, buf, SyncWarp{});
   // v[e] now holds (-1)^k x (row IFFT), k = S::out_idx(t, e); only Omega columns are kept
 
@@ -479,7 +540,8 @@ __device__ __forceinline__ void row_task(const RowArgs& a, int pair0, const floa
 // K4 as one CTA per Omega row over all local coils (chunks of GPC coils), so the channel sum
 // sum_j conj(c_j) u_j (Table 1 "sum c_j") is formed in shared memory in ascending coil order.
 template <int L, int GPC>
-__device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, const float2* tw, float2* xbase, float2* accs) {
+__device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, const float2* tw, float2* xbase, float2* accs,
+                                            bool tw_async = false) {
   using C = Cfg<L>;
   using S = Sched<L>;
   constexpr int T = C::T, E = C::E;
@@ -518,6 +580,7 @@ __device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, const floa
           ++u;
         }
     }
+    if (tw_async && j0 == 0) tw_wait();
     fft<L, +1>(v, t, tw, buf, SyncWarp{});
     __syncthreads();  // accs / previous chunk's exchange buffers are free
     {
@@ -566,16 +629,15 @@ struct RowGeo {
 };
 
 template <int L, int MODE>
-__global__ void __launch_bounds__(256) row_kernel(RowArgs a, const float2* __restrict__ twg) {
+__global__ void __launch_bounds__(256, NLV_MINB) row_kernel(RowArgs a, const float2* __restrict__ twg) {
   extern __shared__ float4 smem_raw[];
   float2* tw = reinterpret_cast<float2*>(smem_raw);
   float2* xb = tw + L;
-  for (int i = threadIdx.x; i < L; i += blockDim.x) tw[i] = twg[i];
-  __syncthreads();
+  tw_copy_async(tw, twg, L);
   if constexpr (MODE == RK_K4)
-    row_task_k4<L, RowGeo<L>::GPC>(a, blockIdx.x, tw, xb, xb + (size_t)L * RowGeo<L>::GPC);
+    row_task_k4<L, RowGeo<L>::GPC>(a, blockIdx.x, tw, xb, xb + (size_t)L * RowGeo<L>::GPC, true);
   else
-    row_task<L, MODE>(a, blockIdx.x * RowGeo<L>::GPC, tw, xb);
+    row_task<L, MODE>(a, blockIdx.x * RowGeo<L>::GPC, tw, xb, true);
 }
 
 // ------------------------------------------------------------------ persistent frame kernel
@@ -637,6 +699,44 @@ __device__ __forceinline__ double2 grid_reduce2(double vr, double vc, double* re
   return tot;
 }
 
+// Publish NV per-CTA partials, barrier, return the CTA-ordered totals (every CTA computes them).
+template <int NV>
+__device__ __forceinline__ void grid_reduceN(const double (&v)[NV], double* red_slot, unsigned* count,
+                                             unsigned* gen, double* sred, double (&tot)[NV]) {
+  double s[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) s[k] = block_sum(v[k], sred);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) red_slot[NV * blockIdx.x + k] = s[k];
+  }
+  grid_barrier(count, gen);
+  __shared__ double stot[8];
+  if (threadIdx.x < 32) {
+    double a[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) a[k] = 0.0;
+    const volatile double* rs = red_slot;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) a[k] += rs[NV * b + k];
+    }
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a[k] += __shfl_xor_sync(0xffffffffu, a[k], o);
+    }
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) stot[k] = a[k];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) tot[k] = stot[k];
+  __syncthreads();
+}
+
 template <int L>
 struct FrameGeo {
   static constexpr int NT = 256;
@@ -649,14 +749,14 @@ struct FrameGeo {
 
 template <int L, int MODE>
 __device__ __forceinline__ void col_phase(const ColArgs& a, const float2* tw, float2* xb, int nslices,
-                                          double& acc_rho, double& acc) {
+                                          double& acc_rho, double& acc, double* acc3) {
   constexpr int NTILE = L / ColGeo<L>::CW;
   const int ntask = NTILE * nslices;
   for (int task = blockIdx.x; task < ntask; task += gridDim.x) {
     // rho slice (j == J, when present) first: its tasks are longer than one coil tile
     const int jj = task / NTILE, tile = task % NTILE;
     const int j = (nslices > a.J) ? (jj == 0 ? a.J : jj - 1) : jj;
-    col_task<L, MODE>(a, tile, j, tw, xb, acc_rho, acc);
+    col_task<L, MODE>(a, tile, j, tw, xb, acc_rho, acc, acc3);
     __syncthreads();  // the next task reuses xb
   }
 }
@@ -670,6 +770,156 @@ __device__ __forceinline__ void row_phase(const RowArgs& a, const float2* tw, fl
     const int ntask = (a.J * (L / 2) + GPC - 1) / GPC;
     for (int task = blockIdx.x; task < ntask; task += gridDim.x) row_task<L, MODE>(a, task * GPC, tw, xb);
   }
+}
+
+// ------------------------------------------------------------------ dataflow CG segment
+// Passes K1..K5 of one CG iteration as a task queue instead of five grid-wide phases: a task
+// waits only for the tasks of the same coil it reads from (per-coil completion counters), so
+// the passes of different coils overlap and no CTA idles at a grid barrier. Task order is
+// pass-major, every dependency points to an earlier ticket, so the queue cannot deadlock.
+__device__ __forceinline__ void wait_ge(const unsigned* ctr, unsigned target) {
+  unsigned spins = 0;
+  while (*(volatile const unsigned*)ctr < target) {
+    __nanosleep(40);
+    if (++spins > (1u << 28)) __trap();
+  }
+}
+
+__device__ __forceinline__ void task_done(unsigned* ctr) {
+  __syncthreads();  // every thread's stores of this task are issued
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+  }
+}
+
+template <int L>
+__device__ __forceinline__ void cg_segment(const FrameArgs& f, ColArgs& ca, RowArgs& ra, const float2* tw,
+                                           float2* xb, double* sred, int g, float alpha) {
+  constexpr int NTILE = L / ColGeo<L>::CW;
+  constexpr int GPC = RowGeo<L>::GPC;
+  constexpr int NRB = (L / 2) / GPC;   // row tasks per coil
+  constexpr size_t N = (size_t)L * L;
+  const int J = f.J;
+  const unsigned gt = (unsigned)(g + 1);
+  unsigned* done = f.done;             // [5][J + 1] cumulative task completions
+  unsigned* qh = f.qhead + (g & 1);
+  const int n1 = NTILE * (J + 1), n2 = NRB * J, n3 = NTILE * J, n4 = NRB * J, n5 = NTILE * J, n5r = 4 * NTILE;
+  const int e1 = n1, e2 = e1 + n2, e3 = e2 + n3, e4 = e3 + n4, e5 = e4 + n5, e6 = e5 + n5r;
+  __shared__ int s_ticket;
+  for (;;) {
+    if (threadIdx.x == 0) s_ticket = (int)atomicAdd(qh, 1u);
+    __syncthreads();
+    const int tk = s_ticket;
+    __syncthreads();
+    if (tk >= e6) break;
+    double d0 = 0.0, d1 = 0.0, a3[4] = {0.0, 0.0, 0.0, 0.0};
+    if (tk < e1) {                                   // K1 (+ fused CG step); rho slice first
+      const int jj = tk / NTILE, tile = tk % NTILE;
+      const int j = (jj == 0) ? J : jj - 1;
+      ca.out = f.tA;
+      col_task<L, CK_IFFT_W_CG>(ca, tile, j, tw, xb, d0, d1, a3);
+      task_done(&done[0 * (J + 1) + j]);
+    } else if (tk < e2) {                            // K2
+      const int t2 = tk - e1, j = t2 / NRB, rb = t2 % NRB;
+      if (threadIdx.x == 0) {
+        wait_ge(&done[0 * (J + 1) + j], gt * NTILE);
+        wait_ge(&done[0 * (J + 1) + J], gt * NTILE);
+        __threadfence();
+      }
+      __syncthreads();
+      ra.in = f.tA;
+      ra.out = f.tB;
+      ra.prho = f.p;
+      row_task<L, RK_K2>(ra, j * (L / 2) + rb * GPC, tw, xb);
+      task_done(&done[1 * (J + 1) + j]);
+    } else if (tk < e3) {                            // K3
+      const int t3 = tk - e2, j = t3 / NTILE, tile = t3 % NTILE;
+      if (threadIdx.x == 0) {
+        wait_ge(&done[1 * (J + 1) + j], gt * NRB);
+        __threadfence();
+      }
+      __syncthreads();
+      ca.in = f.tB;
+      ca.out = f.tA;
+      col_task<L, CK_PSF>(ca, tile, j, tw, xb, d0, d1, a3);
+      task_done(&done[2 * (J + 1) + j]);
+    } else if (tk < e4) {                            // K4 (per-coil channel-sum terms)
+      const int t4 = tk - e3, j = t4 / NRB, rb = t4 % NRB;
+      if (threadIdx.x == 0) {
+        wait_ge(&done[2 * (J + 1) + j], gt * NTILE);
+        __threadfence();
+      }
+      __syncthreads();
+      ra.in = f.tA;
+      ra.out = f.tB;
+      ra.S = f.S_coils;
+      row_task<L, RK_K4>(ra, j * (L / 2) + rb * GPC, tw, xb);
+      task_done(&done[3 * (J + 1) + j]);
+    } else {                                         // K5 coil tiles, then the rho slice
+      const int t5 = tk - e4;
+      int j, tile, rlo = 0, rhi = L;
+      if (t5 < n5) {
+        j = t5 / NTILE;
+        tile = t5 % NTILE;
+        if (threadIdx.x == 0) {
+          wait_ge(&done[3 * (J + 1) + j], gt * NRB);
+          __threadfence();
+        }
+      } else {
+        j = J;
+        tile = (t5 - n5) % NTILE;
+        const int qq = (t5 - n5) / NTILE;
+        rlo = qq * (L / 4);
+        rhi = rlo + L / 4;
+        if (threadIdx.x == 0) {
+          for (int jj = 0; jj < J; ++jj) wait_ge(&done[3 * (J + 1) + jj], gt * NRB);
+          __threadfence();
+        }
+      }
+      __syncthreads();
+      ca.in = f.tB;
+      ca.src2 = f.p + N;
+      ca.out = f.Ap + N;
+      ca.rho_a = f.p;
+      ca.rho_out = f.Ap;
+      ca.S = f.S_coils;
+      ca.nS = J;
+      ca.alpha = alpha;
+      col_task<L, CK_FFT_W_NORMAL>(ca, tile, j, tw, xb, d0, d1, a3, rlo, rhi);
+      // per-task partials, summed later in task order (deterministic under dynamic scheduling)
+      const double sr = block_sum(d0, sred);
+      const double sc = block_sum(d1, sred);
+      if (threadIdx.x == 0) {
+        f.tred[2 * t5] = sr;
+        f.tred[2 * t5 + 1] = sc;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Sum the per-task partials of the K5 tasks in task order (after a grid barrier).
+__device__ __forceinline__ double2 sum_task_partials(const double* tred, int ntask) {
+  __shared__ double2 tot;
+  if (threadIdx.x < 32) {
+    double ar = 0.0, ac = 0.0;
+    const volatile double* rs = tred;
+    for (int b = threadIdx.x; b < ntask; b += 32) {
+      ar += rs[2 * b];
+      ac += rs[2 * b + 1];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ar += __shfl_xor_sync(0xffffffffu, ar, o);
+      ac += __shfl_xor_sync(0xffffffffu, ac, o);
+    }
+    if (threadIdx.x == 0) tot = make_double2(ar, ac);
+  }
+  __syncthreads();
+  const double2 r = tot;
+  __syncthreads();
+  return r;
 }
 
 // optional phase timestamps (CTA 0, after each barrier) for the per-phase breakdown
@@ -691,7 +941,12 @@ __global__ void __launch_bounds__(256, 2) frame_kernel(FrameArgs f) {
   float2* xb = tw + L;
   double* sred = reinterpret_cast<double*>(reinterpret_cast<char*>(xb) + FrameGeo<L>::XB);
   for (int i = threadIdx.x; i < L; i += blockDim.x) tw[i] = f.tw[i];
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < 5 * (f.J + 1); i += blockDim.x) f.done[i] = 0u;
+    if (threadIdx.x < 2) f.qhead[threadIdx.x] = 0u;
+  }
   __syncthreads();
+  grid_barrier(f.bar_count, f.bar_gen);
   int nstamp = 0;
   stamp(f, nstamp);
 
@@ -717,7 +972,7 @@ __global__ void __launch_bounds__(256, 2) frame_kernel(FrameArgs f) {
     // N1: c_j = W^-1 chat_j, column half
     ca.src = f.x + N;
     ca.out = f.tA;
-    col_phase<L, CK_IFFT_W>(ca, tw, xb, J, d0, d1);
+    { double a3[4]; col_phase<L, CK_IFFT_W>(ca, tw, xb, J, d0, d1, a3); }
     grid_barrier(f.bar_count, f.bar_gen);
     stamp(f, nstamp);
     // N2: row half of c_j, c|Omega, rho|Omega, and the row FFT of rho c_j (forward operator)
@@ -731,18 +986,21 @@ __global__ void __launch_bounds__(256, 2) frame_kernel(FrameArgs f) {
     ca.in = f.tB;
     ca.out = f.tA;
     d0 = d1 = 0.0;
-    col_phase<L, CK_RESADJ>(ca, tw, xb, J, d0, d1);
-    double2 res = grid_reduce2(d0, d1, f.red + 0 * 2 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
+    { double a3[4]; col_phase<L, CK_RESADJ>(ca, tw, xb, J, d0, d1, a3); }
+    double2 res = grid_reduce2(d0, d1, f.red + 0 * 6 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
     stamp(f, nstamp);
     if (blockIdx.x == 0 && threadIdx.x == 0) f.scal[SC_RES + nstep] = res.y;
-    // N4: row IFFT -> u, per-coil conj(c) u, conj(rho) u -> row FFT
+    // N4: row IFFT -> u, ordered sum_j conj(c_j) u_j, conj(rho) u -> row FFT
     ra.in = f.tA;
     ra.out = f.tB;
+    ra.S = f.S_all;
     row_phase<L, RK_K4>(ra, tw, xb);
     grid_barrier(f.bar_count, f.bar_gen);
     stamp(f, nstamp);
     // N5: rhs b = DF^H r - alpha (x - x_ref); r = p = b
     ca.in = f.tB;
+    ca.S = f.S_all;
+    ca.nS = 1;
     ca.src = f.x + N;
     ca.src2 = f.xref + N;
     ca.r = f.r + N;
@@ -753,83 +1011,88 @@ __global__ void __launch_bounds__(256, 2) frame_kernel(FrameArgs f) {
     ca.rho_p = f.p;
     ca.alpha = alpha;
     d0 = d1 = 0.0;
-    col_phase<L, CK_FFT_W_RHS>(ca, tw, xb, J + 1, d0, d1);
-    double2 rr2 = grid_reduce2(d0, d1, f.red + 1 * 2 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
+    { double a3[4]; col_phase<L, CK_FFT_W_RHS>(ca, tw, xb, J + 1, d0, d1, a3); }
+    double2 rr2 = grid_reduce2(d0, d1, f.red + 1 * 6 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
     stamp(f, nstamp);
-    double rr = rr2.x + rr2.y, rr_prev = rr;
+    double acc3[4];
+    double rr = rr2.x + rr2.y;   // rr_0
+    float gamma = 0.0f, beta = 0.0f;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       f.scal[SC_RR_RHO] = rr2.x;
       f.scal[SC_RR_CHAT] = rr2.y;
     }
-    // CG
+    // CG: K1 also carries dx += gamma_{i-1} p_{i-1}; the update pass only updates r
     for (int it = 0; it < f.L; ++it) {
-      // P1: p = r + beta p (chat blocks + rho slice), t = w^-1 p -> column IFFT
+      double2 pap;
       ca.r = f.r + N;
       ca.p = f.p + N;
+      ca.dx = f.dx + N;
       ca.rho_r = f.r;
       ca.rho_p = f.p;
-      ca.out = f.tA;
-      ca.beta = (it == 0 || rr_prev == 0.0) ? 0.0f : (float)(rr / rr_prev);
-      col_phase<L, CK_IFFT_W_CG>(ca, tw, xb, J + 1, d0, d1);
-      grid_barrier(f.bar_count, f.bar_gen);
-      stamp(f, nstamp);
-      // P2: K2
-      ra.in = f.tA;
-      ra.out = f.tB;
-      ra.prho = f.p;
-      row_phase<L, RK_K2>(ra, tw, xb);
-      grid_barrier(f.bar_count, f.bar_gen);
-      stamp(f, nstamp);
-      // P3: K3 (PSF convolution)
-      ca.in = f.tB;
-      ca.out = f.tA;
-      col_phase<L, CK_PSF>(ca, tw, xb, J, d0, d1);
-      grid_barrier(f.bar_count, f.bar_gen);
-      stamp(f, nstamp);
-      // P4: K4
-      ra.in = f.tA;
-      ra.out = f.tB;
-      row_phase<L, RK_K4>(ra, tw, xb);
-      grid_barrier(f.bar_count, f.bar_gen);
-      stamp(f, nstamp);
-      // P5: K5 + rho slice: Ap, <p, Ap>
-      ca.in = f.tB;
-      ca.src2 = f.p + N;
-      ca.out = f.Ap + N;
-      ca.rho_a = f.p;
-      ca.rho_out = f.Ap;
-      ca.alpha = alpha;
-      d0 = d1 = 0.0;
-      col_phase<L, CK_FFT_W_NORMAL>(ca, tw, xb, J + 1, d0, d1);
-      double2 pap = grid_reduce2(d0, d1, f.red + 2 * 2 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
-      stamp(f, nstamp);
-      const double papt = pap.x + pap.y;
-      const float gamma = (rr != 0.0) ? (float)(rr / papt) : 0.0f;
+      ca.rho_dx = f.dx;
+      ca.iter = it;
+      ca.gamma = gamma;
+      ca.beta = beta;
+      if (f.dataflow) {
+        // P1..P5 as a per-coil dataflow task queue, then one barrier for <p, Ap>
+        cg_segment<L>(f, ca, ra, tw, xb, sred, nstep * f.L + it, alpha);
+        grid_barrier(f.bar_count, f.bar_gen);
+        pap = sum_task_partials(f.tred, (L / ColGeo<L>::CW) * (J + 4));
+        if (blockIdx.x == 0 && threadIdx.x == 0) f.qhead[(nstep * f.L + it + 1) & 1] = 0u;
+        stamp(f, nstamp);
+      } else {
+        // P1: CG step (dx, p) fused with t = w^-1 p -> column IFFT
+        ca.out = f.tA;
+        col_phase<L, CK_IFFT_W_CG>(ca, tw, xb, J + 1, d0, d1, acc3);
+        grid_barrier(f.bar_count, f.bar_gen);
+        stamp(f, nstamp);
+        // P2: K2
+        ra.in = f.tA;
+        ra.out = f.tB;
+        ra.prho = f.p;
+        row_phase<L, RK_K2>(ra, tw, xb);
+        grid_barrier(f.bar_count, f.bar_gen);
+        stamp(f, nstamp);
+        // P3: K3 (PSF convolution)
+        ca.in = f.tB;
+        ca.out = f.tA;
+        col_phase<L, CK_PSF>(ca, tw, xb, J, d0, d1, acc3);
+        grid_barrier(f.bar_count, f.bar_gen);
+        stamp(f, nstamp);
+        // P4: K4
+        ra.in = f.tA;
+        ra.out = f.tB;
+        ra.S = f.S_all;
+        row_phase<L, RK_K4>(ra, tw, xb);
+        grid_barrier(f.bar_count, f.bar_gen);
+        stamp(f, nstamp);
+        // P5: K5 + rho slice: Ap, <p, Ap>
+        ca.in = f.tB;
+        ca.src2 = f.p + N;
+        ca.out = f.Ap + N;
+        ca.rho_a = f.p;
+        ca.rho_out = f.Ap;
+        ca.S = f.S_all;
+        ca.nS = 1;
+        ca.alpha = alpha;
+        d0 = d1 = 0.0;
+        col_phase<L, CK_FFT_W_NORMAL>(ca, tw, xb, J + 1, d0, d1, acc3);
+        pap = grid_reduce2(d0, d1, f.red + 2 * 6 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
+        stamp(f, nstamp);
+      }
       if (blockIdx.x == 0 && threadIdx.x == 0) {
         f.scal[SC_PAP_RHO + it] = pap.x;
         f.scal[SC_PAP_CHAT + it] = pap.y;
       }
-      // P6: dx += gamma p; r -= gamma Ap; <r, r>   (last iteration: x += dx + gamma p)
-      const bool last = (it == f.L - 1);
-      const long long n2 = (long long)N * (J + 1) / 2, nrho2 = (long long)N / 2;
-      const long long stride = (long long)gridDim.x * blockDim.x;
-      float4* p4 = reinterpret_cast<float4*>(f.p);
-      float4* dx4 = reinterpret_cast<float4*>(f.dx);
-      float4* r4 = reinterpret_cast<float4*>(f.r);
-      float4* x4 = reinterpret_cast<float4*>(f.x);
-      const float4* ap4 = reinterpret_cast<const float4*>(f.Ap);
-      double ar = 0.0, ac = 0.0;
-      for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += stride) {
-        const float4 pv = p4[i];
-        float4 d = (it > 0) ? dx4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-        d.x = fmaf(gamma, pv.x, d.x); d.y = fmaf(gamma, pv.y, d.y);
-        d.z = fmaf(gamma, pv.z, d.z); d.w = fmaf(gamma, pv.w, d.w);
-        if (last) {
-          float4 xv = x4[i];
-          xv.x += d.x; xv.y += d.y; xv.z += d.z; xv.w += d.w;
-          x4[i] = xv;
-        } else {
-          dx4[i] = d;
+      gamma = (rr != 0.0) ? (float)(rr / (pap.x + pap.y)) : 0.0f;
+      if (it < f.L - 1) {
+        // P6: r -= gamma Ap; <r, r>
+        const long long n2 = (long long)N * (J + 1) / 2, nrho2 = (long long)N / 2;
+        const long long stride = (long long)gridDim.x * blockDim.x;
+        float4* r4 = reinterpret_cast<float4*>(f.r);
+        const float4* ap4 = reinterpret_cast<const float4*>(f.Ap);
+        double ar = 0.0, ac = 0.0;
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += stride) {
           const float4 av = ap4[i];
           float4 rv = r4[i];
           rv.x = fmaf(-gamma, av.x, rv.x); rv.y = fmaf(-gamma, av.y, rv.y);
@@ -838,27 +1101,42 @@ __global__ void __launch_bounds__(256, 2) frame_kernel(FrameArgs f) {
           const double sq = (double)rv.x * rv.x + (double)rv.y * rv.y + (double)rv.z * rv.z + (double)rv.w * rv.w;
           if (i < nrho2) ar += sq; else ac += sq;
         }
-      }
-      if (!last) {
-        double2 r2 = grid_reduce2(ar, ac, f.red + 1 * 2 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
+        const double2 r2 = grid_reduce2(ar, ac, f.red + 1 * 6 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
         stamp(f, nstamp);
-        rr_prev = rr;
-        rr = r2.x + r2.y;
+        const double rr_next = r2.x + r2.y;
         if (blockIdx.x == 0 && threadIdx.x == 0) {
           f.scal[SC_RR_RHO + it + 1] = r2.x;
           f.scal[SC_RR_CHAT + it + 1] = r2.y;
         }
-      } else {
-        grid_barrier(f.bar_count, f.bar_gen);
-        stamp(f, nstamp);
+        beta = (rr != 0.0) ? (float)(rr_next / rr) : 0.0f;
+        rr = rr_next;
       }
+    }
+    // Newton update x_{n+1} = x_n + dx, with the last step's gamma p folded in (Eq. 3)
+    {
+      const long long n2 = (long long)N * (J + 1) / 2;
+      const long long stride = (long long)gridDim.x * blockDim.x;
+      const float4* p4 = reinterpret_cast<const float4*>(f.p);
+      const float4* dx4 = reinterpret_cast<const float4*>(f.dx);
+      float4* x4 = reinterpret_cast<float4*>(f.x);
+      const bool hasdx = f.L > 1;
+      for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += stride) {
+        const float4 pv = p4[i];
+        float4 d = hasdx ? dx4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 xv = x4[i];
+        xv.x += fmaf(gamma, pv.x, d.x); xv.y += fmaf(gamma, pv.y, d.y);
+        xv.z += fmaf(gamma, pv.z, d.z); xv.w += fmaf(gamma, pv.w, d.w);
+        x4[i] = xv;
+      }
+      grid_barrier(f.bar_count, f.bar_gen);
+      stamp(f, nstamp);
     }
   }
   if (f.img != nullptr) {
     double d0 = 0.0, d1 = 0.0;
     ca.src = f.x + N;
     ca.out = f.tA;
-    col_phase<L, CK_IFFT_W>(ca, tw, xb, J, d0, d1);
+    { double a3[4]; col_phase<L, CK_IFFT_W>(ca, tw, xb, J, d0, d1, a3); }
     grid_barrier(f.bar_count, f.bar_gen);
     stamp(f, nstamp);
     ra.in = f.tA;

@@ -59,9 +59,14 @@ struct nlinv_plan_s {
   float2 *S_all = nullptr, *S = nullptr, *S_sum = nullptr;   // per-coil terms; local sum; rank sum
   float *rss_all = nullptr, *rss = nullptr, *rss_sum = nullptr;
   double* fred = nullptr;        // frame-kernel reduction partials
+  unsigned* fdone = nullptr;     // dataflow counters: [5][J + 1] completions + [2] queue heads
+  double* ftred = nullptr;       // dataflow per-task partials
+  bool dataflow = true;
   unsigned* fbar = nullptr;      // frame-kernel grid barrier (count, generation)
   bool use_frame = false;
   bool gexec_valid_reset = false;
+  int trace_mode = -1;                    // debug: column mode whose CTA timelines are recorded
+  unsigned long long* trace = nullptr;
   unsigned long long* tstamp = nullptr;   // frame-kernel phase timestamps (nlinv_plan_phase_times)
   double *scal = nullptr, *partials = nullptr;
   unsigned* counter = nullptr;
@@ -224,7 +229,7 @@ static void plan_free(nlinv_plan pl) {
   if (!pl) return;
   void* ptrs[] = {pl->tw, pl->winv, pl->mask, pl->xref, pl->dx, pl->r, pl->p, pl->Ap, pl->tA, pl->tB,
                   pl->c_omega, pl->rho_omega, pl->S_all, pl->S, pl->S_sum, pl->rss_all, pl->rss, pl->rss_sum,
-                  pl->fred, pl->fbar, pl->tstamp, pl->scal, pl->partials,
+                  pl->fred, pl->fbar, pl->fdone, pl->ftred, pl->tstamp, pl->scal, pl->partials,
                   pl->counter, pl->h_frame, pl->h_x, pl->h_img};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -301,13 +306,23 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
     ok &= alloc((void**)&pl->S_sum, sizeof(float2) * pl->Q);
     ok &= alloc((void**)&pl->rss_sum, sizeof(float) * pl->Q);
   }
-  pl->use_frame = (pl->world == 1) && frame_supported(nx) && std::getenv("NLINV_NO_FRAME") == nullptr;
+  // The persistent whole-frame kernel is opt-in (NLINV_FRAME=1): on B200 at C2 the CUDA-graph
+  // multi-kernel path is faster (the single kernel pays instruction-cache misses and spills).
+  {
+    const char* fe = std::getenv("NLINV_FRAME");
+    pl->use_frame = (pl->world == 1) && frame_supported(nx) && fe != nullptr && fe[0] == '1';
+  }
   if (pl->use_frame) {
-    ok &= alloc((void**)&pl->fred, sizeof(double) * 3 * 2 * kMaxFrameBlocks);
+    ok &= alloc((void**)&pl->fred, sizeof(double) * 3 * 6 * kMaxFrameBlocks);
     ok &= alloc((void**)&pl->fbar, sizeof(unsigned) * 2);
+    ok &= alloc((void**)&pl->fdone, sizeof(unsigned) * (5 * (pl->J + 1) + 2));
+    ok &= alloc((void**)&pl->ftred, sizeof(double) * 6 * (size_t)col_tiles(nx) * (pl->J + 4));
+    ok &= alloc((void**)&pl->S_all, sizeof(float2) * pl->Q * pl->J);
+    const char* df = std::getenv("NLINV_DATAFLOW");
+    pl->dataflow = !(df && df[0] == '0');
   }
   ok &= alloc((void**)&pl->scal, sizeof(double) * SC_TOTAL);
-  ok &= alloc((void**)&pl->partials, sizeof(double) * 2 * kMaxRedBlocks);
+  ok &= alloc((void**)&pl->partials, sizeof(double) * 6 * kMaxRedBlocks);
   ok &= alloc((void**)&pl->counter, sizeof(unsigned) * 4);
   if (!ok) {
     plan_free(pl);
@@ -419,6 +434,7 @@ struct Enq {
     return NLINV_OK;
   }
   nlinv_status col(int mode, ColArgs a) {
+    a.trace = (pl->trace_mode == mode) ? pl->trace : nullptr;
     a.winv = pl->winv;
     a.mask = pl->mask;
     a.scal = pl->scal;
@@ -456,10 +472,11 @@ struct Enq {
 #endif
     return NLINV_OK;
   }
-  nlinv_status allreduce_scalar(int slot) {
+  nlinv_status allreduce_scalar(int slot) { return allreduce_scalars(slot, 1); }
+  nlinv_status allreduce_scalars(int slot, int count) {
     if (pl->world == 1) return NLINV_OK;
 #ifdef NLINV_WITH_NCCL
-    NC(ncclAllReduce(pl->scal + slot, pl->scal + slot, 1, ncclDouble, ncclSum, pl->comm, s));
+    NC(ncclAllReduce(pl->scal + slot, pl->scal + slot, count, ncclDouble, ncclSum, pl->comm, s));
 #endif
     return NLINV_OK;
   }
@@ -495,8 +512,10 @@ nlinv_status enq_derivative_head(Enq& q, const float2* dx, bool cg_fused, int it
   if (cg_fused) {
     ca.r = pl->r + pl->N;
     ca.p = pl->p + pl->N;
+    ca.dx = pl->dx + pl->N;
     ca.rho_r = pl->r;
     ca.rho_p = pl->p;
+    ca.rho_dx = pl->dx;
     ca.iter = iter;
     TRY(q.col(CK_IFFT_W_CG, ca));
   } else {
@@ -551,7 +570,7 @@ nlinv_status enq_normal(Enq& q, float alpha, const float2* dx, float2* out, bool
   cb.out_slot = SC_PAP_CHAT + iter;
   cb.out_slot_rho = SC_PAP_RHO + iter;
   TRY(q.col(CK_FFT_W_NORMAL, cb));
-  if (cg) TRY(q.allreduce_scalar(SC_PAP_CHAT + iter));
+  if (cg) TRY(q.allreduce_scalar(SC_PAP_CHAT + iter));   // chat part; the rho part is replicated
   return NLINV_OK;
 }
 
@@ -598,6 +617,11 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
     f.L = L;
     f.alpha0 = pl->prm.alpha0;
     f.q = pl->prm.q;
+    f.dataflow = pl->dataflow ? 1 : 0;
+    f.done = pl->fdone;
+    f.qhead = pl->fdone + 5 * (pl->J + 1);
+    f.tred = pl->ftred;
+    f.S_coils = pl->S_all;
     f.tstamp = pl->tstamp;
     f.tstamp_cap = pl->tstamp ? 8192 : 0;
     return q.kern("frame", [&] { return launch_frame(pl->ng, f, q.s); });
@@ -638,17 +662,22 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
     // CG: L iterations of the normal operator + vector updates
     for (int it = 0; it < L; ++it) {
       TRY(enq_normal(q, alpha, pl->p, pl->Ap, true, it));
-      VecArgs vu = q.vec();
-      vu.x = x;
-      vu.dx = pl->dx;
-      vu.r = pl->r;
-      vu.p = pl->p;
-      vu.Ap = pl->Ap;
-      vu.iter = it;
-      vu.last = (it == L - 1);
-      TRY(q.kern("cg_update", [&] { return launch_cg_update(pl->ng, vu, q.s); }));
-      if (!vu.last) TRY(q.allreduce_scalar(SC_RR_CHAT + it + 1));
+      if (it < L - 1) {  // r -= gamma Ap, <r, r> (dx is updated inside the next K1)
+        VecArgs vr = q.vec();
+        vr.r = pl->r;
+        vr.Ap = pl->Ap;
+        vr.iter = it;
+        TRY(q.kern("r_update", [&] { return launch_r_update(pl->ng, vr, q.s); }));
+        TRY(q.allreduce_scalar(SC_RR_CHAT + it + 1));
+      }
     }
+    // x_{n+1} = x_n + dx (+ gamma_{L-1} p_{L-1}, the step the next K1 would have taken)
+    VecArgs vu = q.vec();
+    vu.x = x;
+    vu.dx = pl->dx;
+    vu.p = pl->p;
+    vu.iter = L;
+    TRY(q.kern("newton_update", [&] { return launch_newton_update(pl->ng, vu, q.s); }));
   }
   if (img) {
     ColArgs ca{};
@@ -953,5 +982,21 @@ extern "C" nlinv_status nlinv_plan_phase_times(nlinv_plan pl, int enable, unsign
   int c = 0;
   while (c < n && out[c] != 0) ++c;
   *count = c;
+  return NLINV_OK;
+}
+
+// ------------------------------------------------------------------ debug CTA timelines (-DNLV_TRACE)
+extern "C" nlinv_status nlinv_plan_trace(nlinv_plan pl, int col_mode, unsigned long long* out, int cap) {
+  if (!pl) return fail(pl, NLINV_ERR_ARG, "NULL plan");
+  if (col_mode >= 0) {
+    if (!pl->trace) CU(cudaMalloc((void**)&pl->trace, sizeof(unsigned long long) * 8 * 8192));
+    CU(cudaMemset(pl->trace, 0, sizeof(unsigned long long) * 8 * 8192));
+    pl->trace_mode = col_mode;
+    return NLINV_OK;
+  }
+  if (!pl->trace || !out) return fail(pl, NLINV_ERR_STATE, "trace not enabled");
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(out, pl->trace, sizeof(unsigned long long) * (cap < 8 * 8192 ? cap : 8 * 8192), cudaMemcpyDeviceToHost));
+  pl->trace_mode = -1;
   return NLINV_OK;
 }

@@ -7,63 +7,45 @@ namespace nlv {
 // ------------------------------------------------------------------ rho-block kernels
 constexpr int kVecThreads = 256;
 
-// CG step: gamma = rr / <p,Ap>; dx += gamma p; r -= gamma Ap; <r,r> (rho, chat partials).
-// Last iteration: x += dx + gamma p (the Newton update x_{n+1} = x_n + dx, Eq. 3).
-__global__ void __launch_bounds__(kVecThreads) cg_update_kernel(VecArgs a) {
+// Newton update after L CG iterations: x += dx + gamma_{L-1} p_{L-1}
+// (dx holds the steps of iterations 0 .. L-2, folded into K1; iter = L).
+__global__ void __launch_bounds__(kVecThreads) newton_update_kernel(VecArgs a) {
+  const float gamma = cg_gamma(a.scal, a.iter - 1);
+  const bool hasdx = a.iter > 1;
+  const long long n2 = a.ntot / 2, stride = (long long)gridDim.x * blockDim.x;
+  const float4* p4 = reinterpret_cast<const float4*>(a.p);
+  const float4* dx4 = reinterpret_cast<const float4*>(a.dx);
+  float4* x4 = reinterpret_cast<float4*>(a.x);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += stride) {
+    const float4 pv = p4[i];
+    const float4 d = hasdx ? dx4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 xv = x4[i];
+    xv.x += fmaf(gamma, pv.x, d.x); xv.y += fmaf(gamma, pv.y, d.y);
+    xv.z += fmaf(gamma, pv.z, d.z); xv.w += fmaf(gamma, pv.w, d.w);
+    x4[i] = xv;
+  }
+}
+
+// CG residual update r_{i+1} = r_i - gamma_i A p_i and <r_{i+1}, r_{i+1}> (rho, chat parts)
+__global__ void __launch_bounds__(kVecThreads) r_update_kernel(VecArgs a) {
   __shared__ double red[32];
   const float gamma = cg_gamma(a.scal, a.iter);
   double acc_rho = 0.0, acc_chat = 0.0;
-  // two complex numbers per 16-byte access; U independent accesses per thread in flight together
-  constexpr int U = 4;
   const long long n2 = a.ntot / 2, stride = (long long)gridDim.x * blockDim.x;
-  const float4* p4 = reinterpret_cast<const float4*>(a.p);
-  float4* dx4 = reinterpret_cast<float4*>(a.dx);
-  float4* r4 = reinterpret_cast<float4*>(a.r);
-  float4* x4 = reinterpret_cast<float4*>(a.x);
   const float4* ap4 = reinterpret_cast<const float4*>(a.Ap);
-  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n2; i0 += U * stride) {
-    float4 pv[U], d[U], w[U], rv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = i0 + u * stride;
-      const bool ok = i < n2;
-      pv[u] = ok ? __ldg(p4 + i) : z4;
-      d[u] = (ok && a.iter > 0) ? dx4[i] : z4;
-      if (a.last) {
-        w[u] = ok ? x4[i] : z4;
-      } else {
-        w[u] = ok ? __ldg(ap4 + i) : z4;
-        rv[u] = ok ? r4[i] : z4;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = i0 + u * stride;
-      if (i >= n2) continue;
-      float4 dd = d[u];
-      dd.x = fmaf(gamma, pv[u].x, dd.x); dd.y = fmaf(gamma, pv[u].y, dd.y);
-      dd.z = fmaf(gamma, pv[u].z, dd.z); dd.w = fmaf(gamma, pv[u].w, dd.w);
-      if (a.last) {
-        float4 xv = w[u];
-        xv.x += dd.x; xv.y += dd.y; xv.z += dd.z; xv.w += dd.w;
-        x4[i] = xv;
-      } else {
-        dx4[i] = dd;
-        float4 r = rv[u];
-        r.x = fmaf(-gamma, w[u].x, r.x); r.y = fmaf(-gamma, w[u].y, r.y);
-        r.z = fmaf(-gamma, w[u].z, r.z); r.w = fmaf(-gamma, w[u].w, r.w);
-        r4[i] = r;
-        const double sq = (double)r.x * r.x + (double)r.y * r.y + (double)r.z * r.z + (double)r.w * r.w;
-        if (2 * i < a.nrho) acc_rho += sq; else acc_chat += sq;
-      }
-    }
+  float4* r4 = reinterpret_cast<float4*>(a.r);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += stride) {
+    const float4 av = ap4[i];
+    float4 rv = r4[i];
+    rv.x = fmaf(-gamma, av.x, rv.x); rv.y = fmaf(-gamma, av.y, rv.y);
+    rv.z = fmaf(-gamma, av.z, rv.z); rv.w = fmaf(-gamma, av.w, rv.w);
+    r4[i] = rv;
+    const double sq = (double)rv.x * rv.x + (double)rv.y * rv.y + (double)rv.z * rv.z + (double)rv.w * rv.w;
+    if (2 * i < a.nrho) acc_rho += sq; else acc_chat += sq;
   }
-  if (!a.last) {
-    const double vv[2] = {acc_rho, acc_chat};
-    const int sl[2] = {SC_RR_RHO + a.iter + 1, SC_RR_CHAT + a.iter + 1};
-    grid_finish<2>(vv, a.partials, a.counter, a.scal_w, sl, red);
-  }
+  const double vv[2] = {acc_rho, acc_chat};
+  const int sl[2] = {SC_RR_RHO + a.iter + 1, SC_RR_CHAT + a.iter + 1};
+  grid_finish<2>(vv, a.partials, a.counter, a.scal_w, sl, red);
 }
 
 // frame output: image = crop_Omega(rho) . sqrt(sum_j |c_j|^2), planes summed in order
@@ -129,8 +111,12 @@ static int vec_grid(long long n) {
   return (int)b;
 }
 
-cudaError_t launch_cg_update(int /*ng*/, const VecArgs& a, cudaStream_t s) {
-  cg_update_kernel<<<vec_grid((a.ntot / 2 + 3) / 4), kVecThreads, 0, s>>>(a);
+cudaError_t launch_r_update(int /*ng*/, const VecArgs& a, cudaStream_t s) {
+  r_update_kernel<<<vec_grid(a.ntot / 2), kVecThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_newton_update(int /*ng*/, const VecArgs& a, cudaStream_t s) {
+  newton_update_kernel<<<vec_grid(a.ntot / 2), kVecThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 __global__ void init_x_kernel(float2* x, long long nrho, long long ntot) {

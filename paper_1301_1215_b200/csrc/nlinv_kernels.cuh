@@ -60,12 +60,16 @@ struct ColArgs {
   unsigned* counter;
   int out_slot;            // scalar index the finished reduction is written to (-1: none)
   int out_slot_rho;        // scalar index of the rho-block partial (FFT_W modes)
-  float beta;              // CG beta for CK_IFFT_W_CG (set by the launcher / frame kernel)
+  float beta;              // CG beta / gamma for CK_IFFT_W_CG (set by the launcher / frame kernel)
+  float gamma;
+  float2* dx;              // CG solution increment (chat blocks), updated in K1
+  float2* rho_dx;
   int nS;                  // number of [n][n] planes of S summed (in order) by the rho slice
   const float2* S;         // coil-sum planes [nS][n][n] (rho slice of the FFT_W modes)
   const float2* rho_a;     // rho-slice operand (p_rho for NORMAL, rho for RHS)
   const float2* rho_b;     // rho_ref for RHS
   float2* rho_out;         // rho-slice output (Ap_rho / adjoint rho)
+  unsigned long long* trace;  // debug timeline (-DNLV_TRACE builds only)
   int iter;                // CG iteration (beta for CK_IFFT_W_CG)
   float alpha;
   int J;
@@ -100,6 +104,12 @@ struct FrameArgs {
   double alpha0, q;
   unsigned long long* tstamp;  // optional per-phase timestamps (ns), CTA 0
   int tstamp_cap;
+  // dataflow CG segment
+  int dataflow;
+  unsigned* done;          // [5][J + 1] cumulative per-coil task completions
+  unsigned* qhead;         // [2] task-queue heads (alternating per CG iteration)
+  double* tred;            // [2 * ntile * (J + 4)] per-task <p, Ap> partials
+  float2* S_coils;         // [J][n][n] per-coil channel-sum terms
 };
 
 struct VecArgs {
@@ -125,7 +135,8 @@ struct VecArgs {
 // launchers (return cudaGetLastError())
 cudaError_t launch_col(int ng, int mode, const ColArgs& a, const float2* tw, cudaStream_t s);
 cudaError_t launch_row(int ng, int mode, const RowArgs& a, const float2* tw, cudaStream_t s);
-cudaError_t launch_cg_update(int ng, const VecArgs& a, cudaStream_t s);
+cudaError_t launch_newton_update(int ng, const VecArgs& a, cudaStream_t s);
+cudaError_t launch_r_update(int ng, const VecArgs& a, cudaStream_t s);
 cudaError_t launch_image(int ng, const float2* rho_omega, const float* rss, int nplanes, float2* img, cudaStream_t s);
 cudaError_t launch_fft2d(int ng, const float2* in, float2* out, int batch, int inverse, const float2* tw,
                          float2* tmp, cudaStream_t s);

@@ -70,6 +70,7 @@ _SIGS = {
     "nlinv_stream_reset": (c_int, [c_void_p]),
     "nlinv_plan_set_profiling": (c_int, [c_void_p, c_int]),
     "nlinv_plan_phase_times": (c_int, [c_void_p, c_int, c_void_p, c_int, ctypes.POINTER(c_int)]),
+    "nlinv_plan_trace": (c_int, [c_void_p, c_int, c_void_p, c_int]),
     "nlinv_plan_profile_json": (c_int, [c_void_p, ctypes.c_char_p, ctypes.c_size_t]),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -279,6 +280,14 @@ class Plan:
         cnt = c_int()
         _check(_lib.nlinv_plan_phase_times(self._h, 0, buf, 8192, ctypes.byref(cnt)), self._h)
         return [buf[i] for i in range(cnt.value)]
+
+    def trace_enable(self, col_mode: int):
+        _check(_lib.nlinv_plan_trace(self._h, int(col_mode), None, 0), self._h)
+
+    def trace_read(self):
+        buf = (ctypes.c_ulonglong * (8 * 8192))()
+        _check(_lib.nlinv_plan_trace(self._h, -1, buf, 8 * 8192), self._h)
+        return np.frombuffer(buf, dtype=np.uint64).reshape(8192, 8).copy()
 
     def stats(self):
         s = Stats()
