@@ -14,6 +14,8 @@
 // Centred unitary DFT (R1): per dimension F_c = (-1)^k FFT((-1)^i .) / sqrt(L) for
 // L % 4 == 0; each 2D transform carries 1/L once.
 #pragma once
+#include <utility>
+
 #include "fft.cuh"
 #include "nlinv_kernels.cuh"
 
@@ -128,6 +130,13 @@ __device__ __forceinline__ float cg_beta(const double* scal, int i) {  // beta_i
   const double rr = cg_rr(scal, i);
   return rr != 0.0 ? (float)(cg_rr(scal, i + 1) / rr) : 0.0f;
 }
+
+// Programmatic dependent launch (PDL): every pass is launched with programmatic stream
+// serialisation, so its CTAs are scheduled while the previous pass drains; pdl_wait() blocks
+// until the previous grid has completed and its memory is visible, so it must precede every
+// read of data produced upstream. pdl_trigger() lets the next pass be scheduled.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
 // Twiddle table global -> shared with cp.async, so its latency overlaps the pass's own loads;
 // the pass waits for it (tw_wait) right before its first transform.
@@ -390,6 +399,8 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColAr
   double* red = reinterpret_cast<double*>(xb + (size_t)L * CW);
   trace_stamp(a.trace, 0);
   tw_copy_async(tw, twg, L);
+  pdl_wait();
+  pdl_trigger();
   if constexpr (MODE == CK_IFFT_W_CG) {
     a.gamma = (a.iter > 0) ? cg_gamma(a.scal, a.iter - 1) : 0.0f;
     a.beta = (a.iter > 0) ? cg_beta(a.scal, a.iter - 1) : 0.0f;
@@ -634,6 +645,8 @@ __global__ void __launch_bounds__(256, NLV_MINB) row_kernel(RowArgs a, const flo
   float2* tw = reinterpret_cast<float2*>(smem_raw);
   float2* xb = tw + L;
   tw_copy_async(tw, twg, L);
+  pdl_wait();
+  pdl_trigger();
   if constexpr (MODE == RK_K4)
     row_task_k4<L, RowGeo<L>::GPC>(a, blockIdx.x, tw, xb, xb + (size_t)L * RowGeo<L>::GPC, true);
   else
@@ -1185,6 +1198,22 @@ static cudaError_t launch_frame_l(const FrameArgs& f, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ dispatch
+template <typename... KArgs, typename... Act>
+static cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Act&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
+}
+
 template <int L, int MODE>
 static cudaError_t launch_col_t(const ColArgs& a, const float2* tw, cudaStream_t s) {
   auto kern = col_kernel<L, MODE>;
@@ -1194,8 +1223,7 @@ static cudaError_t launch_col_t(const ColArgs& a, const float2* tw, cudaStream_t
   const int gy = (MODE == CK_IFFT_W_CG || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ)
                      ? a.J + 1 : a.J;
   dim3 grid(L / ColGeo<L>::CW, gy);
-  kern<<<grid, ColGeo<L>::THREADS, smem, s>>>(a, tw);
-  return cudaGetLastError();
+  return launch_k(kern, grid, dim3(ColGeo<L>::THREADS), smem, s, a, tw);
 }
 
 template <int L>
@@ -1221,8 +1249,7 @@ static cudaError_t launch_row_t(const RowArgs& a, const float2* tw, cudaStream_t
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int grid = (MODE == RK_K4) ? L / 2 : (a.J * (L / 2) + RowGeo<L>::GPC - 1) / RowGeo<L>::GPC;
-  kern<<<grid, RowGeo<L>::THREADS, smem, s>>>(a, tw);
-  return cudaGetLastError();
+  return launch_k(kern, dim3(grid), dim3(RowGeo<L>::THREADS), smem, s, a, tw);
 }
 
 template <int L>

@@ -1,8 +1,18 @@
 // Non-templated kernels (rho block, CG vector update, frame output) and the grid-size
 // dispatch of the templated FFT-pass kernels (kernels_impl.cuh, one TU per size in inst.cu).
+#include <cstdlib>
+
 #include "kernels_impl.cuh"
 
 namespace nlv {
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("NLINV_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 // ------------------------------------------------------------------ rho-block kernels
 constexpr int kVecThreads = 256;
@@ -10,6 +20,8 @@ constexpr int kVecThreads = 256;
 // Newton update after L CG iterations: x += dx + gamma_{L-1} p_{L-1}
 // (dx holds the steps of iterations 0 .. L-2, folded into K1; iter = L).
 __global__ void __launch_bounds__(kVecThreads) newton_update_kernel(VecArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const float gamma = cg_gamma(a.scal, a.iter - 1);
   const bool hasdx = a.iter > 1;
   const long long n2 = a.ntot / 2, stride = (long long)gridDim.x * blockDim.x;
@@ -29,6 +41,8 @@ __global__ void __launch_bounds__(kVecThreads) newton_update_kernel(VecArgs a) {
 // CG residual update r_{i+1} = r_i - gamma_i A p_i and <r_{i+1}, r_{i+1}> (rho, chat parts)
 __global__ void __launch_bounds__(kVecThreads) r_update_kernel(VecArgs a) {
   __shared__ double red[32];
+  pdl_wait();
+  pdl_trigger();
   const float gamma = cg_gamma(a.scal, a.iter);
   double acc_rho = 0.0, acc_chat = 0.0;
   const long long n2 = a.ntot / 2, stride = (long long)gridDim.x * blockDim.x;
@@ -51,6 +65,7 @@ __global__ void __launch_bounds__(kVecThreads) r_update_kernel(VecArgs a) {
 // frame output: image = crop_Omega(rho) . sqrt(sum_j |c_j|^2), planes summed in order
 __global__ void image_kernel(const float2* __restrict__ rho_omega, const float* __restrict__ rss, int nplanes,
                              float2* img, int Q) {
+  pdl_wait();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Q; i += gridDim.x * blockDim.x) {
     float s = 0.f;
     for (int j = 0; j < nplanes; ++j) s += rss[(size_t)j * Q + i];
@@ -60,6 +75,7 @@ __global__ void image_kernel(const float2* __restrict__ rho_omega, const float* 
 
 // local coil sums before the cross-rank all-reduce (world > 1)
 __global__ void coil_sum_kernel(const float2* __restrict__ S_all, int J, float2* S, int Q) {
+  pdl_wait();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Q; i += gridDim.x * blockDim.x) {
     float2 s = make_float2(0.f, 0.f);
     for (int j = 0; j < J; ++j) s = cadd(s, S_all[(size_t)j * Q + i]);
@@ -67,6 +83,7 @@ __global__ void coil_sum_kernel(const float2* __restrict__ S_all, int J, float2*
   }
 }
 __global__ void rss_sum_kernel(const float* __restrict__ rss_all, int J, float* rss, int Q) {
+  pdl_wait();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Q; i += gridDim.x * blockDim.x) {
     float s = 0.f;
     for (int j = 0; j < J; ++j) s += rss_all[(size_t)j * Q + i];
@@ -112,20 +129,18 @@ static int vec_grid(long long n) {
 }
 
 cudaError_t launch_r_update(int /*ng*/, const VecArgs& a, cudaStream_t s) {
-  r_update_kernel<<<vec_grid(a.ntot / 2), kVecThreads, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_k(r_update_kernel, dim3(vec_grid(a.ntot / 2)), dim3(kVecThreads), 0, s, a);
 }
 cudaError_t launch_newton_update(int /*ng*/, const VecArgs& a, cudaStream_t s) {
-  newton_update_kernel<<<vec_grid(a.ntot / 2), kVecThreads, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_k(newton_update_kernel, dim3(vec_grid(a.ntot / 2)), dim3(kVecThreads), 0, s, a);
 }
 __global__ void init_x_kernel(float2* x, long long nrho, long long ntot) {
+  pdl_wait();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ntot; i += (long long)gridDim.x * blockDim.x)
     x[i] = make_float2(i < nrho ? 1.0f : 0.0f, 0.0f);
 }
 cudaError_t launch_init_x(float2* x, long long nrho, long long ntot, cudaStream_t s) {
-  init_x_kernel<<<vec_grid(ntot), kVecThreads, 0, s>>>(x, nrho, ntot);
-  return cudaGetLastError();
+  return launch_k(init_x_kernel, dim3(vec_grid(ntot)), dim3(kVecThreads), 0, s, x, nrho, ntot);
 }
 
 int col_tiles(int ng) {
@@ -137,18 +152,15 @@ int col_tiles(int ng) {
 
 cudaError_t launch_image(int ng, const float2* rho_omega, const float* rss, int nplanes, float2* img, cudaStream_t s) {
   const int Q = (ng / 2) * (ng / 2);
-  image_kernel<<<(Q + 255) / 256, 256, 0, s>>>(rho_omega, rss, nplanes, img, Q);
-  return cudaGetLastError();
+  return launch_k(image_kernel, dim3((Q + 255) / 256), dim3(256), 0, s, rho_omega, rss, nplanes, img, Q);
 }
 cudaError_t launch_coil_sum(int ng, const float2* S_all, int J, float2* S, cudaStream_t s) {
   const int Q = (ng / 2) * (ng / 2);
-  coil_sum_kernel<<<(Q + 255) / 256, 256, 0, s>>>(S_all, J, S, Q);
-  return cudaGetLastError();
+  return launch_k(coil_sum_kernel, dim3((Q + 255) / 256), dim3(256), 0, s, S_all, J, S, Q);
 }
 cudaError_t launch_rss_sum(int ng, const float* rss_all, int J, float* rss, cudaStream_t s) {
   const int Q = (ng / 2) * (ng / 2);
-  rss_sum_kernel<<<(Q + 255) / 256, 256, 0, s>>>(rss_all, J, rss, Q);
-  return cudaGetLastError();
+  return launch_k(rss_sum_kernel, dim3((Q + 255) / 256), dim3(256), 0, s, rss_all, J, rss, Q);
 }
 cudaError_t launch_frame(int ng, const FrameArgs& f, cudaStream_t s) {
 #define X(L) if (ng == L) return launch_frame_##L(f, s);
