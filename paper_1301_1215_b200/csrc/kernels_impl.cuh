@@ -102,24 +102,20 @@ __device__ __forceinline__ void grid_finish(const double (&v)[NV], double* parti
   }
   __syncthreads();
   if (is_last) {
-    __threadfence();
-    if (threadIdx.x < 32) {
+    __threadfence();  // gpu-scope fence: also invalidates this SM's L1, the partials are read fresh
 #pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        double acc = 0.0;
-        const volatile double* pv = partials + k * kMaxRedBlocks;
-        for (unsigned i = threadIdx.x; i < nblk; i += 32) acc += pv[i];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (threadIdx.x == 0 && slot[k] >= 0) scal_w[slot[k]] = acc;
-      }
-      if (threadIdx.x == 0) *counter = 0u;
+    for (int k = 0; k < NV; ++k) {
+      // every thread of the last CTA sums a fixed strided subset, then the fixed block tree
+      double acc = 0.0;
+      const double* pk = partials + k * kMaxRedBlocks;
+      for (unsigned i = threadIdx.x; i < nblk; i += blockDim.x) acc += __ldcg(pk + i);
+      const double tot = block_sum(acc, red);
+      if (threadIdx.x == 0 && slot[k] >= 0) scal_w[slot[k]] = tot;
     }
+    if (threadIdx.x == 0) *counter = 0u;
   }
 }
 
-// Textbook CG scalars (R9): gamma_i = rr_i / <p_i, A p_i>, beta_i = rr_{i+1} / rr_i.
-// rr_i and <p_i, A p_i> are published as (rho, chat) parts; rho is replicated and counted once.
 __device__ __forceinline__ double cg_rr(const double* scal, int i) { return scal[SC_RR_RHO + i] + scal[SC_RR_CHAT + i]; }
 __device__ __forceinline__ float cg_gamma(const double* scal, int i) {
   const double rr = cg_rr(scal, i);
@@ -225,6 +221,48 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
       }
       if (tw_async) asm volatile("cp.async.wait_all;\n" ::);
       return;
+    }
+  }
+
+  // rho block spread over the coil tiles (a.rho_spread): tile (j, tile) also handles a contiguous
+  // stripe of the N rho elements, so the pass needs no extra CTAs (one wave at 2 CTAs/SM)
+  if constexpr (MODE == CK_IFFT_W_CG || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ) {
+    if (a.rho_spread) {
+      constexpr int NTILE = L / CW;
+      const int nstripe = a.J * NTILE, stripe = j * NTILE + tile;
+      const size_t chunk = (N + nstripe - 1) / nstripe;
+      const size_t lo = (size_t)stripe * chunk, hi = (lo + chunk < N) ? lo + chunk : N;
+      for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        if constexpr (MODE == CK_IFFT_W_CG) {
+          const float2 rv = a.rho_r[i], pv = a.rho_p[i];
+          if (a.iter > 0) {
+            const float2 dv = (a.iter > 1) ? a.rho_dx[i] : make_float2(0.f, 0.f);
+            a.rho_dx[i] = make_float2(fmaf(a.gamma, pv.x, dv.x), fmaf(a.gamma, pv.y, dv.y));
+          }
+          a.rho_p[i] = make_float2(fmaf(a.beta, pv.x, rv.x), fmaf(a.beta, pv.y, rv.y));
+        } else {
+          const int y = (int)(i / L), xx = (int)(i % L);
+          float2 sv = make_float2(0.f, 0.f);
+          if (xx >= q && xx < q + n && y >= q && y < q + n) {
+            const size_t o = (size_t)(y - q) * n + (xx - q);
+            for (int sp = 0; sp < a.nS; ++sp) sv = cadd(sv, a.S[sp * Qs + o]);
+          }
+          if constexpr (MODE == CK_FFT_W_NORMAL) {
+            const float2 pv = a.rho_a[i];
+            const float2 o = make_float2(fmaf(a.alpha, pv.x, sv.x), fmaf(a.alpha, pv.y, sv.y));
+            a.rho_out[i] = o;
+            acc_rho += (double)pv.x * o.x + (double)pv.y * o.y;
+          } else if constexpr (MODE == CK_FFT_W_RHS) {
+            const float2 d = csub(a.rho_a[i], a.rho_b[i]);
+            const float2 b = make_float2(fmaf(-a.alpha, d.x, sv.x), fmaf(-a.alpha, d.y, sv.y));
+            a.rho_r[i] = b;
+            a.rho_p[i] = b;
+            acc_rho += (double)b.x * b.x + (double)b.y * b.y;
+          } else {
+            a.rho_out[i] = sv;
+          }
+        }
+      }
     }
   }
 
@@ -408,7 +446,7 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColAr
   double acc_rho = 0.0, acc = 0.0;
   // the rho slice (when present) is blockIdx.y == 0 so it is scheduled first
   const bool has_rho = (MODE == CK_IFFT_W_CG || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ);
-  const int j = has_rho ? (blockIdx.y == 0 ? a.J : (int)blockIdx.y - 1) : (int)blockIdx.y;
+  const int j = (has_rho && !a.rho_spread) ? (blockIdx.y == 0 ? a.J : (int)blockIdx.y - 1) : (int)blockIdx.y;
   double acc3[4] = {0.0, 0.0, 0.0, 0.0};
   col_task<L, MODE>(a, blockIdx.x, j, tw, xb, acc_rho, acc, acc3, 0, L, true);
   trace_stamp(a.trace, 5);
@@ -550,9 +588,9 @@ __device__ __forceinline__ void row_task(const RowArgs& a, int pair0, const floa
 
 // K4 as one CTA per Omega row over all local coils (chunks of GPC coils), so the channel sum
 // sum_j conj(c_j) u_j (Table 1 "sum c_j") is formed in shared memory in ascending coil order.
-template <int L, int GPC>
-__device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, const float2* tw, float2* xbase, float2* accs,
-                                            bool tw_async = false) {
+template <int L>
+__device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, int jlo, int jhi, int plane, const float2* tw,
+                                            float2* xbase, float2* accs, bool tw_async = false) {
   using C = Cfg<L>;
   using S = Sched<L>;
   constexpr int T = C::T, E = C::E;
@@ -560,7 +598,7 @@ __device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, const floa
   constexpr size_t H = (size_t)n * L, Q = (size_t)n * n;
   constexpr float invL = 1.0f / (float)L;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int g = tid / T, t = tid % T;
+  const int g = tid / T, t = tid % T, GPC = nt / T;
   const int row = q + yy;
   RowBuf buf{xbase + (size_t)g * L};
   for (int i = tid; i < n; i += nt) accs[i] = make_float2(0.f, 0.f);
@@ -572,9 +610,9 @@ __device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, const floa
     for (int e = 0; e < E; ++e)
       if (out_is_omega<L>(e)) rv[u++] = a.rho_omega[(size_t)yy * n + (S::out_idx(t, e) - q)];
   }
-  for (int j0 = 0; j0 < a.J; j0 += GPC) {
+  for (int j0 = jlo; j0 < jhi; j0 += GPC) {
     const int j = j0 + g;
-    const bool active = j < a.J;
+    const bool active = j < jhi;
     float2 v[E], cv[E / 2];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -591,7 +629,7 @@ __device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, const floa
           ++u;
         }
     }
-    if (tw_async && j0 == 0) tw_wait();
+    if (tw_async && j0 == jlo) tw_wait();
     fft<L, +1>(v, t, tw, buf, SyncWarp{});
     __syncthreads();  // accs / previous chunk's exchange buffers are free
     {
@@ -612,7 +650,7 @@ __device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, const floa
     __syncthreads();
     for (int xx = tid; xx < n; xx += nt) {
       float2 sacc = accs[xx];
-      for (int gg = 0; gg < GPC && j0 + gg < a.J; ++gg) sacc = cadd(sacc, xbase[(size_t)gg * L + xx]);
+      for (int gg = 0; gg < GPC && j0 + gg < jhi; ++gg) sacc = cadd(sacc, xbase[(size_t)gg * L + xx]);
       accs[xx] = sacc;
     }
     __syncthreads();
@@ -627,8 +665,18 @@ __device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, const floa
     }
   }
   __syncthreads();
-  for (int i = tid; i < n; i += nt) a.S[(size_t)yy * n + i] = accs[i];
+  for (int i = tid; i < n; i += nt) a.S[(size_t)plane * Q + (size_t)yy * n + i] = accs[i];
   __syncthreads();
+}
+
+// K4 coils per CTA: 64-thread CTAs (whole warps) so the n Omega rows x coil chunks fill the SMs
+int k4_chunk_override();  // NLINV_K4CHUNK (0 = default)
+template <int L>
+inline int k4_chunk_t(int J) {
+  const int o = k4_chunk_override();
+  int c = (o > 0) ? o : 256 / Cfg<L>::T;
+  if (c * Cfg<L>::T > 1024) c = 1024 / Cfg<L>::T;
+  return c < J ? c : J;
 }
 
 template <int L>
@@ -647,8 +695,11 @@ __global__ void __launch_bounds__(256, NLV_MINB) row_kernel(RowArgs a, const flo
   tw_copy_async(tw, twg, L);
   pdl_wait();
   pdl_trigger();
-  if constexpr (MODE == RK_K4)
-    row_task_k4<L, RowGeo<L>::GPC>(a, blockIdx.x, tw, xb, xb + (size_t)L * RowGeo<L>::GPC, true);
+  if constexpr (MODE == RK_K4) {
+    // CTA = (Omega row, chunk of a.kchunk coils); chunk c writes coil-sum plane c
+    const int jlo = blockIdx.y * a.kchunk, jhi = min(a.J, jlo + a.kchunk);
+    row_task_k4<L>(a, blockIdx.x, jlo, jhi, blockIdx.y, tw, xb, xb + (size_t)L * (blockDim.x / Cfg<L>::T), true);
+  }
   else
     row_task<L, MODE>(a, blockIdx.x * RowGeo<L>::GPC, tw, xb, true);
 }
@@ -778,7 +829,8 @@ template <int L, int MODE>
 __device__ __forceinline__ void row_phase(const RowArgs& a, const float2* tw, float2* xb) {
   constexpr int GPC = RowGeo<L>::GPC;
   if constexpr (MODE == RK_K4) {
-    for (int yy = blockIdx.x; yy < L / 2; yy += gridDim.x) row_task_k4<L, GPC>(a, yy, tw, xb, xb + (size_t)L * GPC);
+    for (int yy = blockIdx.x; yy < L / 2; yy += gridDim.x)
+      row_task_k4<L>(a, yy, 0, a.J, 0, tw, xb, xb + (size_t)L * GPC);
   } else {
     const int ntask = (a.J * (L / 2) + GPC - 1) / GPC;
     for (int task = blockIdx.x; task < ntask; task += gridDim.x) row_task<L, MODE>(a, task * GPC, tw, xb);
@@ -1220,8 +1272,8 @@ static cudaError_t launch_col_t(const ColArgs& a, const float2* tw, cudaStream_t
   const size_t smem = ColGeo<L>::SMEM;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int gy = (MODE == CK_IFFT_W_CG || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ)
-                     ? a.J + 1 : a.J;
+  const int gy = ((MODE == CK_IFFT_W_CG || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ) &&
+                  !a.rho_spread) ? a.J + 1 : a.J;
   dim3 grid(L / ColGeo<L>::CW, gy);
   return launch_k(kern, grid, dim3(ColGeo<L>::THREADS), smem, s, a, tw);
 }
@@ -1243,13 +1295,22 @@ static cudaError_t launch_col_l(int mode, const ColArgs& a, const float2* tw, cu
 }
 
 template <int L, int MODE>
-static cudaError_t launch_row_t(const RowArgs& a, const float2* tw, cudaStream_t s) {
+static cudaError_t launch_row_t(const RowArgs& a0, const float2* tw, cudaStream_t s) {
   const size_t smem = RowGeo<L>::SMEM;
   auto kern = row_kernel<L, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int grid = (MODE == RK_K4) ? L / 2 : (a.J * (L / 2) + RowGeo<L>::GPC - 1) / RowGeo<L>::GPC;
-  return launch_k(kern, dim3(grid), dim3(RowGeo<L>::THREADS), smem, s, a, tw);
+  if constexpr (MODE == RK_K4) {
+    RowArgs a = a0;
+    a.kchunk = k4_chunk_t<L>(a.J);
+    const size_t sm4 = sizeof(float2) * ((size_t)L * (a.kchunk + 1) + L / 2);
+    if (sm4 > smem && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4)) != cudaSuccess)
+      return e;
+    return launch_k(kern, dim3(L / 2, (a.J + a.kchunk - 1) / a.kchunk), dim3(a.kchunk * Cfg<L>::T), sm4, s, a, tw);
+  } else {
+    const int grid = (a0.J * (L / 2) + RowGeo<L>::GPC - 1) / RowGeo<L>::GPC;
+    return launch_k(kern, dim3(grid), dim3(RowGeo<L>::THREADS), smem, s, a0, tw);
+  }
 }
 
 template <int L>

@@ -66,6 +66,7 @@ struct nlinv_plan_s {
   bool use_frame = false;
   bool gexec_valid_reset = false;
   int trace_mode = -1;                    // debug: column mode whose CTA timelines are recorded
+  bool rho_spread = true;                 // rho block in stripes over the coil tiles (NLINV_RHO_SPREAD=0: own CTAs)
   unsigned long long* trace = nullptr;
   unsigned long long* tstamp = nullptr;   // frame-kernel phase timestamps (nlinv_plan_phase_times)
   double *scal = nullptr, *partials = nullptr;
@@ -300,6 +301,7 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
   ok &= alloc((void**)&pl->c_omega, sizeof(float2) * pl->Q * pl->J);
   ok &= alloc((void**)&pl->rho_omega, sizeof(float2) * pl->Q);
   ok &= alloc((void**)&pl->S, sizeof(float2) * pl->Q);
+  ok &= alloc((void**)&pl->S_all, sizeof(float2) * pl->Q * pl->J);
   ok &= alloc((void**)&pl->rss_all, sizeof(float) * pl->Q * pl->J);
   if (pl->world > 1) {
     ok &= alloc((void**)&pl->rss, sizeof(float) * pl->Q);
@@ -309,6 +311,10 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
   // The persistent whole-frame kernel is opt-in (NLINV_FRAME=1): on B200 at C2 the CUDA-graph
   // multi-kernel path is faster (the single kernel pays instruction-cache misses and spills).
   {
+    const char* rs = std::getenv("NLINV_RHO_SPREAD");
+    pl->rho_spread = !(rs && rs[0] == '0');
+  }
+  {
     const char* fe = std::getenv("NLINV_FRAME");
     pl->use_frame = (pl->world == 1) && frame_supported(nx) && fe != nullptr && fe[0] == '1';
   }
@@ -317,7 +323,6 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
     ok &= alloc((void**)&pl->fbar, sizeof(unsigned) * 2);
     ok &= alloc((void**)&pl->fdone, sizeof(unsigned) * (5 * (pl->J + 1) + 2));
     ok &= alloc((void**)&pl->ftred, sizeof(double) * 6 * (size_t)col_tiles(nx) * (pl->J + 4));
-    ok &= alloc((void**)&pl->S_all, sizeof(float2) * pl->Q * pl->J);
     const char* df = std::getenv("NLINV_DATAFLOW");
     pl->dataflow = !(df && df[0] == '0');
   }
@@ -435,6 +440,7 @@ struct Enq {
   }
   nlinv_status col(int mode, ColArgs a) {
     a.trace = (pl->trace_mode == mode) ? pl->trace : nullptr;
+    a.rho_spread = pl->rho_spread ? 1 : 0;
     a.winv = pl->winv;
     a.mask = pl->mask;
     a.scal = pl->scal;
@@ -537,16 +543,25 @@ nlinv_status enq_k4_allreduce(Enq& q) {
   RowArgs ra{};
   ra.in = pl->tA;
   ra.out = pl->tB;
-  ra.S = pl->S;
+  ra.S = pl->S_all;   // one plane per K4 coil chunk
   TRY(q.row(RK_K4, ra));
-  TRY(q.allreduce_f((const float*)pl->S, (float*)pl->S_sum, 2 * pl->Q));
+  if (pl->world > 1) {
+    const int np = k4_planes(pl->ng, pl->J);
+    TRY(q.kern("coil_sum", [&] { return launch_coil_sum(pl->ng, pl->S_all, np, pl->S, q.s); }));
+    TRY(q.allreduce_f((const float*)pl->S, (float*)pl->S_sum, 2 * pl->Q));
+  }
   return NLINV_OK;
 }
 
-// the coil-sum plane the rho slices read (local, or rank-summed for world > 1)
+// the coil-sum planes the rho slices add up (chunk planes in order, or the rank-summed plane)
 void set_S(nlinv_plan pl, ColArgs& c) {
-  c.S = (pl->world > 1) ? pl->S_sum : pl->S;
-  c.nS = 1;
+  if (pl->world > 1) {
+    c.S = pl->S_sum;
+    c.nS = 1;
+  } else {
+    c.S = pl->S_all;
+    c.nS = k4_planes(pl->ng, pl->J);
+  }
 }
 
 // out = (DF^H DF + alpha) dx; with_cg: the CG-fused variant on the plan's p (iteration iter)

@@ -6,6 +6,21 @@
 
 namespace nlv {
 
+int k4_chunk_override() {
+  static const int v = [] {
+    const char* e = std::getenv("NLINV_K4CHUNK");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
+int k4_planes(int ng, int J) {
+#define X(L) if (ng == L) { const int c = k4_chunk_t<L>(J); return (J + c - 1) / c; }
+  NLV_FOR_EACH_NG(X)
+#undef X
+  return J;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("NLINV_PDL");
@@ -122,7 +137,7 @@ cudaError_t launch_fft2d(int ng, const float2* in, float2* out, int batch, int i
 
 static int vec_grid(long long n) {
   long long b = (n + kVecThreads - 1) / kVecThreads;
-  const long long cap = 148 * 8;
+  const long long cap = 148 * 4;
   if (b > cap) b = cap;
   if (b < 1) b = 1;
   return (int)b;

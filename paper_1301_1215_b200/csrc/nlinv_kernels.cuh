@@ -70,6 +70,7 @@ struct ColArgs {
   const float2* rho_b;     // rho_ref for RHS
   float2* rho_out;         // rho-slice output (Ap_rho / adjoint rho)
   unsigned long long* trace;  // debug timeline (-DNLV_TRACE builds only)
+  int rho_spread;          // 1: the rho block is processed in stripes by the coil tiles (no rho CTAs)
   int iter;                // CG iteration (beta for CK_IFFT_W_CG)
   float alpha;
   int J;
@@ -82,10 +83,12 @@ struct RowArgs {
   float2* rho_omega;       // [n][n]
   const float2* xrho;      // rho of the point, full grid (set point)
   const float2* prho;      // rho part of the direction, full grid (K2)
-  float2* S;               // [J][n][n] per-coil terms conj(c_j) u_j (K4)
+  float2* S;               // K4: coil-sum planes [chunks][n][n] (ordered within a chunk)
   float* rss;              // [J][n][n] per-coil |c_j|^2 (RSS)
   int J;
+  int kchunk;              // K4 coils per CTA (set by the launcher)
 };
+int k4_planes(int ng, int J);  // number of K4 coil-sum planes
 
 // Persistent whole-frame kernel (world == 1): every buffer of the plan.
 constexpr int kMaxFrameBlocks = 1024;
