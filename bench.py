@@ -56,6 +56,9 @@ def algo_bytes(name: str, ng: int, Jl: int, L: int = CG) -> float:
         "col_psf": 8 * Jl * N + N,
         "row_k4": 10 * Jl * N + 4 * N,
         "col_fft_w_normal": 20 * Jl * N + 4 * N + 18 * N,   # + rho slice: S, p_rho in, Ap_rho out
+        # K5 fused with the CG residual update (cooperative): T4, p, w^-1, r in, r out per coil;
+        # rho stripe: S, p_rho in, Ap_rho out and back in, r_rho in and out
+        "col_fft_w_normal_upd": 32 * Jl * N + 4 * N + 50 * N,
         "r_update": 24 * N * (Jl + 1),                       # r, Ap in; r out
         "newton_update": 32 * N * (Jl + 1),                  # p, dx, x in; x out
         "col_ifft_w": 8 * Jl * N + 4 * N + 4 * Jl * N,

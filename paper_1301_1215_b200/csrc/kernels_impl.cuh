@@ -116,6 +116,30 @@ __device__ __forceinline__ void grid_finish(const double (&v)[NV], double* parti
   }
 }
 
+// Sense-reversing barrier over nb co-resident CTAs (cooperative launch guarantees residency).
+__device__ __forceinline__ void grid_barrier_n(unsigned* count, unsigned* gen, unsigned nb) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = *(volatile unsigned*)gen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == nb - 1) {
+      *count = 0u;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      unsigned spins = 0;
+      while (*(volatile unsigned*)gen == g) {
+        __nanosleep(20);
+        if (++spins > (1u << 28)) __trap();  // never hang the GPU: abort the context instead
+      }
+    }
+    __threadfence();  // acquire; gpu-scope fence also invalidates this SM's L1
+  }
+  __syncthreads();
+}
+
+// Textbook CG scalars (R9): gamma_i = rr_i / <p_i, A p_i>, beta_i = rr_{i+1} / rr_i.
+// rr_i and <p_i, A p_i> are published as (rho, chat) parts; rho is replicated and counted once.
 __device__ __forceinline__ double cg_rr(const double* scal, int i) { return scal[SC_RR_RHO + i] + scal[SC_RR_CHAT + i]; }
 __device__ __forceinline__ float cg_gamma(const double* scal, int i) {
   const double rr = cg_rr(scal, i);
@@ -409,7 +433,8 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
         if constexpr (MODE == CK_FFT_W_NORMAL) {
           const float2 pv = o1[u];
           const float2 o = make_float2(fmaf(a.alpha, pv.x, val.x), fmaf(a.alpha, pv.y, val.y));
-          a.out[j * N + i] = o;
+          if (a.fuse_update) v[e0 + u] = o;   // A p stays in registers for the fused r update
+          else a.out[j * N + i] = o;
           acc += (double)pv.x * o.x + (double)pv.y * o.y;
         } else if constexpr (MODE == CK_FFT_W_RHS) {
           const float2 d = csub(o1[u], o2[u]);
@@ -419,6 +444,66 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
           acc += (double)b.x * b.x + (double)b.y * b.y;
         } else {
           a.out[j * N + i] = val;
+        }
+      }
+    }
+    if constexpr (MODE == CK_FFT_W_NORMAL) {
+      if (a.fuse_update) {
+        // K5 + CG residual update in one cooperative pass (world == 1): publish <p,Ap>, grid
+        // barrier, every CTA forms gamma from the partials in CTA order, then r -= gamma Ap on
+        // its own tile (A p still in registers) and its rho stripe; <r,r> goes to the last CTA.
+        const unsigned nb = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
+        double* sred = reinterpret_cast<double*>(xb);   // the exchange buffer is free here
+        __syncthreads();
+        const double pr = block_sum(acc_rho, sred);
+        const double pc = block_sum(acc, sred);
+        if (threadIdx.x == 0) {
+          a.fpart[2 * bid] = pr;
+          a.fpart[2 * bid + 1] = pc;
+        }
+        grid_barrier_n(a.bar_count, a.bar_gen, nb);
+        double tr = 0.0, tc = 0.0;
+        for (unsigned b = threadIdx.x; b < nb; b += blockDim.x) {
+          tr += __ldcg(a.fpart + 2 * b);
+          tc += __ldcg(a.fpart + 2 * b + 1);
+        }
+        tr = block_sum(tr, sred);
+        tc = block_sum(tc, sred);
+        __shared__ double s_pap[2];
+        if (threadIdx.x == 0) {
+          s_pap[0] = tr;
+          s_pap[1] = tc;
+          if (bid == 0) {
+            a.scal_w[SC_PAP_RHO + a.iter] = tr;
+            a.scal_w[SC_PAP_CHAT + a.iter] = tc;
+          }
+        }
+        __syncthreads();
+        if (!a.last_iter) {
+          const double rr = cg_rr(a.scal, a.iter);
+          const float gamma = (rr != 0.0) ? (float)(rr / (s_pap[0] + s_pap[1])) : 0.0f;
+          double ar = 0.0, ac = 0.0;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const size_t i = j * N + (size_t)S::out_idx(t, e) * L + x;
+            float2 rv = a.r[i];
+            rv = make_float2(fmaf(-gamma, v[e].x, rv.x), fmaf(-gamma, v[e].y, rv.y));
+            a.r[i] = rv;
+            ac += (double)rv.x * rv.x + (double)rv.y * rv.y;
+          }
+          constexpr int NTILE = L / CW;
+          const int nstripe = a.J * NTILE, stripe = j * NTILE + tile;
+          const size_t chunk = (N + nstripe - 1) / nstripe;
+          const size_t lo = (size_t)stripe * chunk, hi = (lo + chunk < N) ? lo + chunk : N;
+          for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+            const float2 av = a.rho_out[i];
+            float2 rv = a.rho_r[i];
+            rv = make_float2(fmaf(-gamma, av.x, rv.x), fmaf(-gamma, av.y, rv.y));
+            a.rho_r[i] = rv;
+            ar += (double)rv.x * rv.x + (double)rv.y * rv.y;
+          }
+          acc_rho = ar;   // handed back to the caller for the <r,r> last-CTA reduction
+          acc = ac;
         }
       }
     }
@@ -451,7 +536,13 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColAr
   col_task<L, MODE>(a, blockIdx.x, j, tw, xb, acc_rho, acc, acc3, 0, L, true);
   trace_stamp(a.trace, 5);
   if constexpr (MODE == CK_RESADJ || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_NORMAL) {
-    if (a.partials != nullptr) {
+    if (MODE == CK_FFT_W_NORMAL && a.fuse_update) {
+      if (!a.last_iter) {  // <r_{i+1}, r_{i+1}> after the fused update
+        const double vv[2] = {acc_rho, acc};
+        const int sl[2] = {SC_RR_RHO + a.iter + 1, SC_RR_CHAT + a.iter + 1};
+        grid_finish<2>(vv, a.partials, a.counter, a.scal_w, sl, red);
+      }
+    } else if (a.partials != nullptr) {
       const double vv[2] = {acc_rho, acc};
       const int sl[2] = {a.out_slot_rho, a.out_slot};
       grid_finish<2>(vv, a.partials, a.counter, a.scal_w, sl, red);
@@ -671,6 +762,15 @@ __device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, int jlo, i
 
 // K4 coils per CTA: 64-thread CTAs (whole warps) so the n Omega rows x coil chunks fill the SMs
 int k4_chunk_override();  // NLINV_K4CHUNK (0 = default)
+int row_pairs_override(); // NLINV_ROWPAIRS (0 = default)
+template <int L>
+inline int row_pairs_per_cta() {
+  const int o = row_pairs_override();
+  int g = (o > 0) ? o : 256 / Cfg<L>::T;
+  if (g > 256 / Cfg<L>::T) g = 256 / Cfg<L>::T;
+  while ((g * Cfg<L>::T) % 32 != 0) ++g;
+  return g;
+}
 template <int L>
 inline int k4_chunk_t(int J) {
   const int o = k4_chunk_override();
@@ -701,7 +801,7 @@ __global__ void __launch_bounds__(256, NLV_MINB) row_kernel(RowArgs a, const flo
     row_task_k4<L>(a, blockIdx.x, jlo, jhi, blockIdx.y, tw, xb, xb + (size_t)L * (blockDim.x / Cfg<L>::T), true);
   }
   else
-    row_task<L, MODE>(a, blockIdx.x * RowGeo<L>::GPC, tw, xb, true);
+    row_task<L, MODE>(a, blockIdx.x * (blockDim.x / Cfg<L>::T), tw, xb, true);
 }
 
 // ------------------------------------------------------------------ persistent frame kernel
@@ -1266,6 +1366,35 @@ static cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
 }
 
+template <typename... KArgs, typename... Act>
+static cudaError_t launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                               Act&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
+}
+
+// can the K5 pass run as one co-resident (cooperative) wave with the fused r update?
+template <int L>
+static bool col_fusable_l(int J) {
+  auto kern = col_kernel<L, CK_FFT_W_NORMAL>;
+  const size_t smem = ColGeo<L>::SMEM;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return false;
+  int dev = 0, nsm = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, ColGeo<L>::THREADS, smem) != cudaSuccess) return false;
+  return (long long)(L / ColGeo<L>::CW) * J <= (long long)per * nsm;
+}
+
 template <int L, int MODE>
 static cudaError_t launch_col_t(const ColArgs& a, const float2* tw, cudaStream_t s) {
   auto kern = col_kernel<L, MODE>;
@@ -1275,6 +1404,7 @@ static cudaError_t launch_col_t(const ColArgs& a, const float2* tw, cudaStream_t
   const int gy = ((MODE == CK_IFFT_W_CG || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ) &&
                   !a.rho_spread) ? a.J + 1 : a.J;
   dim3 grid(L / ColGeo<L>::CW, gy);
+  if (MODE == CK_FFT_W_NORMAL && a.fuse_update) return launch_coop(kern, grid, dim3(ColGeo<L>::THREADS), smem, s, a, tw);
   return launch_k(kern, grid, dim3(ColGeo<L>::THREADS), smem, s, a, tw);
 }
 
@@ -1308,8 +1438,9 @@ static cudaError_t launch_row_t(const RowArgs& a0, const float2* tw, cudaStream_
       return e;
     return launch_k(kern, dim3(L / 2, (a.J + a.kchunk - 1) / a.kchunk), dim3(a.kchunk * Cfg<L>::T), sm4, s, a, tw);
   } else {
-    const int grid = (a0.J * (L / 2) + RowGeo<L>::GPC - 1) / RowGeo<L>::GPC;
-    return launch_k(kern, dim3(grid), dim3(RowGeo<L>::THREADS), smem, s, a0, tw);
+    const int gpc = row_pairs_per_cta<L>();
+    const int grid = (a0.J * (L / 2) + gpc - 1) / gpc;
+    return launch_k(kern, dim3(grid), dim3(gpc * Cfg<L>::T), smem, s, a0, tw);
   }
 }
 
@@ -1423,7 +1554,8 @@ static cudaError_t launch_fft2d_l(const float2* in, float2* out, int batch, int 
                                cudaStream_t s);                                                 \
   int col_tiles_##L();                                                                          \
   cudaError_t launch_frame_##L(const FrameArgs& f, cudaStream_t s);                             \
-  bool frame_ok_##L();
+  bool frame_ok_##L();                                                                          \
+  bool col_fusable_##L(int J);
 #define NLV_INSTANTIATE(L)                                                                       \
   cudaError_t launch_col_##L(int mode, const ColArgs& a, const float2* tw, cudaStream_t s) {    \
     return launch_col_l<L>(mode, a, tw, s);                                                      \
@@ -1437,7 +1569,8 @@ static cudaError_t launch_fft2d_l(const float2* in, float2* out, int batch, int 
   }                                                                                              \
   int col_tiles_##L() { return L / ColGeo<L>::CW; }                                             \
   cudaError_t launch_frame_##L(const FrameArgs& f, cudaStream_t s) { return launch_frame_l<L>(f, s); } \
-  bool frame_ok_##L() { return FrameGeo<L>::kOk; }
+  bool frame_ok_##L() { return FrameGeo<L>::kOk; }                                              \
+  bool col_fusable_##L(int J) { return col_fusable_l<L>(J); }
 
 #define NLV_FOR_EACH_NG(X) X(16) X(32) X(48) X(64) X(96) X(128) X(192) X(256) X(384) X(512) X(768) X(1024)
 NLV_FOR_EACH_NG(NLV_DECLARE)

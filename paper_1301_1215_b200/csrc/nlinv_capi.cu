@@ -67,6 +67,9 @@ struct nlinv_plan_s {
   bool gexec_valid_reset = false;
   int trace_mode = -1;                    // debug: column mode whose CTA timelines are recorded
   bool rho_spread = true;                 // rho block in stripes over the coil tiles (NLINV_RHO_SPREAD=0: own CTAs)
+  bool fuse_k5 = false;                   // K5 + r update as one cooperative pass (world == 1, fits one wave)
+  unsigned* kbar = nullptr;               // its grid barrier
+  double* kpart = nullptr;                // its <p, Ap> partials
   unsigned long long* trace = nullptr;
   unsigned long long* tstamp = nullptr;   // frame-kernel phase timestamps (nlinv_plan_phase_times)
   double *scal = nullptr, *partials = nullptr;
@@ -230,7 +233,7 @@ static void plan_free(nlinv_plan pl) {
   if (!pl) return;
   void* ptrs[] = {pl->tw, pl->winv, pl->mask, pl->xref, pl->dx, pl->r, pl->p, pl->Ap, pl->tA, pl->tB,
                   pl->c_omega, pl->rho_omega, pl->S_all, pl->S, pl->S_sum, pl->rss_all, pl->rss, pl->rss_sum,
-                  pl->fred, pl->fbar, pl->fdone, pl->ftred, pl->tstamp, pl->scal, pl->partials,
+                  pl->fred, pl->fbar, pl->fdone, pl->ftred, pl->tstamp, pl->kbar, pl->kpart, pl->scal, pl->partials,
                   pl->counter, pl->h_frame, pl->h_x, pl->h_img};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -313,6 +316,12 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
   {
     const char* rs = std::getenv("NLINV_RHO_SPREAD");
     pl->rho_spread = !(rs && rs[0] == '0');
+    const char* fk = std::getenv("NLINV_FUSE_K5");
+    pl->fuse_k5 = pl->rho_spread && pl->world == 1 && !(fk && fk[0] == '0') && col_fusable(nx, pl->J);
+    if (pl->fuse_k5) {
+      ok &= alloc((void**)&pl->kbar, sizeof(unsigned) * 2);
+      ok &= alloc((void**)&pl->kpart, sizeof(double) * 2 * kMaxRedBlocks);
+    }
   }
   {
     const char* fe = std::getenv("NLINV_FRAME");
@@ -356,6 +365,7 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
   if (e == cudaSuccess) e = cudaMemset(pl->scal, 0, sizeof(double) * SC_TOTAL);
   if (e == cudaSuccess) e = cudaMemset(pl->counter, 0, sizeof(unsigned) * 4);
   if (e == cudaSuccess && pl->fbar) e = cudaMemset(pl->fbar, 0, sizeof(unsigned) * 2);
+  if (e == cudaSuccess && pl->kbar) e = cudaMemset(pl->kbar, 0, sizeof(unsigned) * 2);
   if (e != cudaSuccess) {
     std::string msg = std::string("plan upload: ") + cudaGetErrorString(e);
     plan_free(pl);
@@ -447,7 +457,8 @@ struct Enq {
     a.scal_w = pl->scal;
     a.counter = pl->counter;
     a.J = pl->J;
-    return kern(kColNames[mode], [&] { return launch_col(pl->ng, mode, a, pl->tw, s); });
+    const char* name = (mode == CK_FFT_W_NORMAL && a.fuse_update) ? "col_fft_w_normal_upd" : kColNames[mode];
+    return kern(name, [&] { return launch_col(pl->ng, mode, a, pl->tw, s); });
   }
   nlinv_status row(int mode, RowArgs a) {
     a.J = pl->J;
@@ -565,7 +576,7 @@ void set_S(nlinv_plan pl, ColArgs& c) {
 }
 
 // out = (DF^H DF + alpha) dx; with_cg: the CG-fused variant on the plan's p (iteration iter)
-nlinv_status enq_normal(Enq& q, float alpha, const float2* dx, float2* out, bool cg, int iter) {
+nlinv_status enq_normal(Enq& q, float alpha, const float2* dx, float2* out, bool cg, int iter, int last_iter = -1) {
   nlinv_plan pl = q.pl;
   TRY(enq_derivative_head(q, dx, cg, iter));
   ColArgs ca{};
@@ -584,6 +595,16 @@ nlinv_status enq_normal(Enq& q, float alpha, const float2* dx, float2* out, bool
   cb.partials = cg ? pl->partials : nullptr;
   cb.out_slot = SC_PAP_CHAT + iter;
   cb.out_slot_rho = SC_PAP_RHO + iter;
+  if (cg && pl->fuse_k5) {
+    cb.fuse_update = 1;
+    cb.last_iter = (iter == last_iter) ? 1 : 0;
+    cb.r = pl->r + pl->N;
+    cb.rho_r = pl->r;
+    cb.bar_count = pl->kbar;
+    cb.bar_gen = pl->kbar + 1;
+    cb.fpart = pl->kpart;
+    cb.iter = iter;
+  }
   TRY(q.col(CK_FFT_W_NORMAL, cb));
   if (cg) TRY(q.allreduce_scalar(SC_PAP_CHAT + iter));   // chat part; the rho part is replicated
   return NLINV_OK;
@@ -676,8 +697,8 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
     TRY(q.allreduce_scalar(SC_RR_CHAT + 0));
     // CG: L iterations of the normal operator + vector updates
     for (int it = 0; it < L; ++it) {
-      TRY(enq_normal(q, alpha, pl->p, pl->Ap, true, it));
-      if (it < L - 1) {  // r -= gamma Ap, <r, r> (dx is updated inside the next K1)
+      TRY(enq_normal(q, alpha, pl->p, pl->Ap, true, it, L - 1));
+      if (it < L - 1 && !pl->fuse_k5) {  // r -= gamma Ap, <r, r> (dx is updated inside the next K1)
         VecArgs vr = q.vec();
         vr.r = pl->r;
         vr.Ap = pl->Ap;

@@ -14,6 +14,14 @@ int k4_chunk_override() {
   return v;
 }
 
+int row_pairs_override() {
+  static const int v = [] {
+    const char* e = std::getenv("NLINV_ROWPAIRS");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 int k4_planes(int ng, int J) {
 #define X(L) if (ng == L) { const int c = k4_chunk_t<L>(J); return (J + c - 1) / c; }
   NLV_FOR_EACH_NG(X)
@@ -182,6 +190,12 @@ cudaError_t launch_frame(int ng, const FrameArgs& f, cudaStream_t s) {
   NLV_FOR_EACH_NG(X)
 #undef X
   return cudaErrorInvalidValue;
+}
+bool col_fusable(int ng, int J) {
+#define X(L) if (ng == L) return col_fusable_##L(J);
+  NLV_FOR_EACH_NG(X)
+#undef X
+  return false;
 }
 bool frame_supported(int ng) {
 #define X(L) if (ng == L) return frame_ok_##L();

@@ -71,6 +71,11 @@ struct ColArgs {
   float2* rho_out;         // rho-slice output (Ap_rho / adjoint rho)
   unsigned long long* trace;  // debug timeline (-DNLV_TRACE builds only)
   int rho_spread;          // 1: the rho block is processed in stripes by the coil tiles (no rho CTAs)
+  int fuse_update;         // K5: cooperative pass that also does r -= gamma A p and <r, r> (world == 1)
+  int last_iter;           // K5 fused: last CG iteration (no r update needed)
+  unsigned* bar_count;     // grid barrier of the fused K5
+  unsigned* bar_gen;
+  double* fpart;           // [2 * blocks] <p, Ap> partials of the fused K5
   int iter;                // CG iteration (beta for CK_IFFT_W_CG)
   float alpha;
   int J;
@@ -149,6 +154,7 @@ int col_tiles(int ng);  // column-kernel CTAs per coil
 cudaError_t launch_init_x(float2* x, long long nrho, long long ntot, cudaStream_t s);
 cudaError_t launch_frame(int ng, const FrameArgs& f, cudaStream_t s);
 bool frame_supported(int ng);
+bool col_fusable(int ng, int J);
 cudaError_t launch_coil_sum(int ng, const float2* S_all, int J, float2* S, cudaStream_t s);
 cudaError_t launch_rss_sum(int ng, const float* rss_all, int J, float* rss, cudaStream_t s);
 
