@@ -59,6 +59,12 @@ def algo_bytes(name: str, ng: int, Jl: int, L: int = CG) -> float:
         # K5 fused with the CG residual update (cooperative): T4, p, w^-1, r in, r out per coil;
         # rho stripe: S, p_rho in, Ap_rho out and back in, r_rho in and out
         "col_fft_w_normal_upd": 32 * Jl * N + 4 * N + 50 * N,
+        # ... + beta and K1 of the next iteration on the same tile (p, dx in; p, dx, T1 out)
+        "col_k5_cg_k1": 72 * Jl * N + 4 * N + 74 * N,
+        # ... last iteration: + the Newton update x += dx + gamma p (p, dx, x in; x out)
+        "col_k5_newton": 48 * Jl * N + 4 * N + 50 * N,
+        # Newton rhs + K1 of CG iteration 0 (T1 out)
+        "col_rhs_k1": 4 * Jl * N + 8 * Jl * N + 8 * Jl * N + 4 * N + 16 * Jl * N + 34 * N + 4 * Jl * N,
         "r_update": 24 * N * (Jl + 1),                       # r, Ap in; r out
         "newton_update": 32 * N * (Jl + 1),                  # p, dx, x in; x out
         "col_ifft_w": 8 * Jl * N + 4 * N + 4 * Jl * N,

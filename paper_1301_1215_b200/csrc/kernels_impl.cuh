@@ -441,6 +441,7 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
           const float2 b = make_float2(fmaf(-a.alpha, d.x, val.x), fmaf(-a.alpha, d.y, val.y));
           a.r[j * N + i] = b;
           a.p[j * N + i] = b;
+          v[e0 + u] = b;   // kept for the fused K1 of iteration 0
           acc += (double)b.x * b.x + (double)b.y * b.y;
         } else {
           a.out[j * N + i] = val;
@@ -479,9 +480,36 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
           }
         }
         __syncthreads();
-        if (!a.last_iter) {
-          const double rr = cg_rr(a.scal, a.iter);
-          const float gamma = (rr != 0.0) ? (float)(rr / (s_pap[0] + s_pap[1])) : 0.0f;
+        const double rr = cg_rr(a.scal, a.iter);
+        const float gamma = (rr != 0.0) ? (float)(rr / (s_pap[0] + s_pap[1])) : 0.0f;
+        constexpr int NTILE = L / CW;
+        const int nstripe = a.J * NTILE, stripe = j * NTILE + tile;
+        const size_t chunk = (N + nstripe - 1) / nstripe;
+        const size_t lo = (size_t)stripe * chunk, hi = (lo + chunk < N) ? lo + chunk : N;
+        if (a.last_iter) {
+          if (a.fuse_newton) {
+            // Newton update x_{n+1} = x_n + dx + gamma_{L-1} p_{L-1} (Eq. 3) on this tile and stripe
+            const bool hasdx = a.iter > 0;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              const size_t i = j * N + (size_t)S::out_idx(t, e) * L + x;
+              const float2 pv = a.src2[i];
+              const float2 dv = hasdx ? a.dx[i] : make_float2(0.f, 0.f);
+              float2 xv = a.xc[i];
+              xv.x += fmaf(gamma, pv.x, dv.x);
+              xv.y += fmaf(gamma, pv.y, dv.y);
+              a.xc[i] = xv;
+            }
+            for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+              const float2 pv = a.rho_a[i];
+              const float2 dv = hasdx ? a.rho_dx[i] : make_float2(0.f, 0.f);
+              float2 xv = a.x_rho[i];
+              xv.x += fmaf(gamma, pv.x, dv.x);
+              xv.y += fmaf(gamma, pv.y, dv.y);
+              a.x_rho[i] = xv;
+            }
+          }
+        } else {
           double ar = 0.0, ac = 0.0;
 #pragma unroll
           for (int e = 0; e < E; ++e) {
@@ -489,12 +517,9 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
             float2 rv = a.r[i];
             rv = make_float2(fmaf(-gamma, v[e].x, rv.x), fmaf(-gamma, v[e].y, rv.y));
             a.r[i] = rv;
+            v[e] = rv;   // r_{i+1}, reused by the fused K1 below
             ac += (double)rv.x * rv.x + (double)rv.y * rv.y;
           }
-          constexpr int NTILE = L / CW;
-          const int nstripe = a.J * NTILE, stripe = j * NTILE + tile;
-          const size_t chunk = (N + nstripe - 1) / nstripe;
-          const size_t lo = (size_t)stripe * chunk, hi = (lo + chunk < N) ? lo + chunk : N;
           for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
             const float2 av = a.rho_out[i];
             float2 rv = a.rho_r[i];
@@ -502,8 +527,101 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
             a.rho_r[i] = rv;
             ar += (double)rv.x * rv.x + (double)rv.y * rv.y;
           }
-          acc_rho = ar;   // handed back to the caller for the <r,r> last-CTA reduction
-          acc = ac;
+          if (!a.fuse_k1) {
+            acc_rho = ar;   // handed back to the caller for the <r,r> last-CTA reduction
+            acc = ac;
+          } else {
+            // second barrier: <r_{i+1}, r_{i+1}> -> beta_i, then K1 of iteration i+1 on the same tile:
+            // dx += gamma_i p_i; p_{i+1} = r_{i+1} + beta_i p_i; t = w^-1 p_{i+1} -> column IFFT
+            const double rr_r = block_sum(ar, sred);
+            const double rr_c = block_sum(ac, sred);
+            if (threadIdx.x == 0) {
+              a.fpart[2 * nb + 2 * bid] = rr_r;
+              a.fpart[2 * nb + 2 * bid + 1] = rr_c;
+            }
+            grid_barrier_n(a.bar_count, a.bar_gen, nb);
+            double ur = 0.0, uc = 0.0;
+            for (unsigned b2 = threadIdx.x; b2 < nb; b2 += blockDim.x) {
+              ur += __ldcg(a.fpart + 2 * nb + 2 * b2);
+              uc += __ldcg(a.fpart + 2 * nb + 2 * b2 + 1);
+            }
+            ur = block_sum(ur, sred);
+            uc = block_sum(uc, sred);
+            __shared__ double s_rr[2];
+            if (threadIdx.x == 0) {
+              s_rr[0] = ur;
+              s_rr[1] = uc;
+              if (bid == 0) {
+                a.scal_w[SC_RR_RHO + a.iter + 1] = ur;
+                a.scal_w[SC_RR_CHAT + a.iter + 1] = uc;
+              }
+            }
+            __syncthreads();
+            const float beta = (rr != 0.0) ? (float)((s_rr[0] + s_rr[1]) / rr) : 0.0f;
+            const bool hasdx = a.iter > 0;
+            constexpr int CH = 8;
+#pragma unroll
+            for (int e0 = 0; e0 < E; e0 += CH) {
+              float wv[CH];
+              float2 pv[CH], dv[CH];
+#pragma unroll
+              for (int u = 0; u < CH; ++u) {
+                const size_t ii = (size_t)S::out_idx(t, e0 + u) * L + x;
+                wv[u] = a.winv[ii];
+                pv[u] = a.src2[j * N + ii];
+                dv[u] = hasdx ? a.dx[j * N + ii] : make_float2(0.f, 0.f);
+              }
+#pragma unroll
+              for (int u = 0; u < CH; ++u) {
+                const int k = S::out_idx(t, e0 + u);
+                const size_t i = j * N + (size_t)k * L + x;
+                a.dx[i] = make_float2(fmaf(gamma, pv[u].x, dv[u].x), fmaf(gamma, pv[u].y, dv[u].y));
+                const float2 pn = make_float2(fmaf(beta, pv[u].x, v[e0 + u].x), fmaf(beta, pv[u].y, v[e0 + u].y));
+                a.p[i] = pn;
+                v[e0 + u] = cscale(pn, wv[u] * sgn_of(k));
+              }
+            }
+            for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+              const float2 pv = a.rho_a[i], rv = a.rho_r[i];
+              const float2 dv = hasdx ? a.rho_dx[i] : make_float2(0.f, 0.f);
+              a.rho_dx[i] = make_float2(fmaf(gamma, pv.x, dv.x), fmaf(gamma, pv.y, dv.y));
+              a.rho_p[i] = make_float2(fmaf(beta, pv.x, rv.x), fmaf(beta, pv.y, rv.y));
+            }
+            __syncthreads();   // the reduction scratch (xb) becomes the transform's exchange buffer
+            out_to_in<L>(v, t, buf, SyncBlock{});
+            fft<L, +1>(v, t, tw, buf, SyncBlock{});
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              if (out_is_omega<L>(e)) {
+                const int k = S::out_idx(t, e);
+                a.t1[j * H + (size_t)(k - q) * L + x] = cscale(v[e], invL * sgn_of(k));
+              }
+            }
+            acc_rho = acc = 0.0;
+          }
+        }
+      }
+    }
+  }
+  // Newton rhs fused with K1 of CG iteration 0 (p_0 = r_0 = b): t = w^-1 b -> column IFFT
+  if constexpr (MODE == CK_FFT_W_RHS) {
+    if (a.fuse_k1) {
+      constexpr int CH = 8;
+#pragma unroll
+      for (int e0 = 0; e0 < E; e0 += CH) {
+        float wv[CH];
+#pragma unroll
+        for (int u = 0; u < CH; ++u) wv[u] = a.winv[(size_t)S::out_idx(t, e0 + u) * L + x];
+#pragma unroll
+        for (int u = 0; u < CH; ++u) v[e0 + u] = cscale(v[e0 + u], wv[u] * sgn_of(S::out_idx(t, e0 + u)));
+      }
+      out_to_in<L>(v, t, buf, SyncBlock{});
+      fft<L, +1>(v, t, tw, buf, SyncBlock{});
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if (out_is_omega<L>(e)) {
+          const int k = S::out_idx(t, e);
+          a.t1[j * H + (size_t)(k - q) * L + x] = cscale(v[e], invL * sgn_of(k));
         }
       }
     }
@@ -537,7 +655,7 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColAr
   trace_stamp(a.trace, 5);
   if constexpr (MODE == CK_RESADJ || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_NORMAL) {
     if (MODE == CK_FFT_W_NORMAL && a.fuse_update) {
-      if (!a.last_iter) {  // <r_{i+1}, r_{i+1}> after the fused update
+      if (!a.last_iter && !a.fuse_k1) {  // <r_{i+1}, r_{i+1}> after the fused update
         const double vv[2] = {acc_rho, acc};
         const int sl[2] = {SC_RR_RHO + a.iter + 1, SC_RR_CHAT + a.iter + 1};
         grid_finish<2>(vv, a.partials, a.counter, a.scal_w, sl, red);

@@ -68,6 +68,7 @@ struct nlinv_plan_s {
   int trace_mode = -1;                    // debug: column mode whose CTA timelines are recorded
   bool rho_spread = true;                 // rho block in stripes over the coil tiles (NLINV_RHO_SPREAD=0: own CTAs)
   bool fuse_k5 = false;                   // K5 + r update as one cooperative pass (world == 1, fits one wave)
+  bool fuse_k1 = false;                   // ... also K1 of the next iteration / the Newton update
   unsigned* kbar = nullptr;               // its grid barrier
   double* kpart = nullptr;                // its <p, Ap> partials
   unsigned long long* trace = nullptr;
@@ -320,7 +321,9 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
     pl->fuse_k5 = pl->rho_spread && pl->world == 1 && !(fk && fk[0] == '0') && col_fusable(nx, pl->J);
     if (pl->fuse_k5) {
       ok &= alloc((void**)&pl->kbar, sizeof(unsigned) * 2);
-      ok &= alloc((void**)&pl->kpart, sizeof(double) * 2 * kMaxRedBlocks);
+      ok &= alloc((void**)&pl->kpart, sizeof(double) * 4 * kMaxRedBlocks);
+      const char* f1 = std::getenv("NLINV_FUSE_K1");
+      pl->fuse_k1 = !(f1 && f1[0] == '0');
     }
   }
   {
@@ -457,7 +460,10 @@ struct Enq {
     a.scal_w = pl->scal;
     a.counter = pl->counter;
     a.J = pl->J;
-    const char* name = (mode == CK_FFT_W_NORMAL && a.fuse_update) ? "col_fft_w_normal_upd" : kColNames[mode];
+    const char* name = kColNames[mode];
+    if (mode == CK_FFT_W_NORMAL && a.fuse_update)
+      name = a.fuse_k1 ? "col_k5_cg_k1" : (a.fuse_newton ? "col_k5_newton" : "col_fft_w_normal_upd");
+    if (mode == CK_FFT_W_RHS && a.fuse_k1) name = "col_rhs_k1";
     return kern(name, [&] { return launch_col(pl->ng, mode, a, pl->tw, s); });
   }
   nlinv_status row(int mode, RowArgs a) {
@@ -693,8 +699,58 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
     cb.rho_b = pl->xref;
     cb.rho_r = pl->r;
     cb.rho_p = pl->p;
+    if (pl->fuse_k1) {  // K1 of CG iteration 0 (p_0 = b) folded into the rhs pass
+      cb.fuse_k1 = 1;
+      cb.t1 = pl->tA;
+    }
     TRY(q.col(CK_FFT_W_RHS, cb));
     TRY(q.allreduce_scalar(SC_RR_CHAT + 0));
+    if (pl->fuse_k1) {
+      // CG, fused form: per iteration K2, K3, K4 and one cooperative pass that does K5,
+      // gamma, r -= gamma Ap, <r,r>, beta and K1 of the next iteration (or the Newton update)
+      for (int it = 0; it < L; ++it) {
+        RowArgs ra{};
+        ra.in = pl->tA;
+        ra.out = pl->tB;
+        ra.prho = pl->p;
+        TRY(q.row(RK_K2, ra));
+        ColArgs c3{};
+        c3.in = pl->tB;
+        c3.out = pl->tA;
+        TRY(q.col(CK_PSF, c3));
+        TRY(enq_k4_allreduce(q));
+        ColArgs c5{};
+        c5.in = pl->tB;
+        c5.src2 = pl->p + N;
+        c5.out = pl->Ap + N;
+        set_S(pl, c5);
+        c5.rho_a = pl->p;
+        c5.rho_out = pl->Ap;
+        c5.alpha = alpha;
+        c5.partials = pl->partials;
+        c5.out_slot = SC_PAP_CHAT + it;
+        c5.out_slot_rho = SC_PAP_RHO + it;
+        c5.fuse_update = 1;
+        c5.last_iter = (it == L - 1) ? 1 : 0;
+        c5.fuse_k1 = (it < L - 1) ? 1 : 0;
+        c5.fuse_newton = (it == L - 1) ? 1 : 0;
+        c5.iter = it;
+        c5.r = pl->r + N;
+        c5.rho_r = pl->r;
+        c5.p = pl->p + N;
+        c5.rho_p = pl->p;
+        c5.dx = pl->dx + N;
+        c5.rho_dx = pl->dx;
+        c5.t1 = pl->tA;
+        c5.xc = x + N;
+        c5.x_rho = x;
+        c5.bar_count = pl->kbar;
+        c5.bar_gen = pl->kbar + 1;
+        c5.fpart = pl->kpart;
+        TRY(q.col(CK_FFT_W_NORMAL, c5));
+      }
+      continue;
+    }
     // CG: L iterations of the normal operator + vector updates
     for (int it = 0; it < L; ++it) {
       TRY(enq_normal(q, alpha, pl->p, pl->Ap, true, it, L - 1));

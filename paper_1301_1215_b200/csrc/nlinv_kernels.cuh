@@ -75,7 +75,12 @@ struct ColArgs {
   int last_iter;           // K5 fused: last CG iteration (no r update needed)
   unsigned* bar_count;     // grid barrier of the fused K5
   unsigned* bar_gen;
-  double* fpart;           // [2 * blocks] <p, Ap> partials of the fused K5
+  double* fpart;           // [4 * blocks] <p, Ap> and <r, r> partials of the fused K5
+  int fuse_k1;             // fused K5 / rhs: also run K1 of the next CG iteration (T1 into t1)
+  int fuse_newton;         // fused K5, last iteration: also x += dx + gamma p
+  float2* t1;              // K1 output (half image) for the fused variants
+  float2* xc;              // unknowns, chat blocks (fused Newton update)
+  float2* x_rho;           // unknowns, rho block
   int iter;                // CG iteration (beta for CK_IFFT_W_CG)
   float alpha;
   int J;
