@@ -259,3 +259,39 @@ def test_reconstruct_c2_full_frame():
     st = plan.stats()
     assert np.allclose(st["residual"], hist, rtol=1e-3)
     plan.close()
+
+
+VARIANTS = {
+    "fused (default)": {},
+    "unfused K1/K5": {"NLINV_FUSE_K1": "0", "NLINV_FUSE_K5": "0"},
+    "K5+update only": {"NLINV_FUSE_K1": "0"},
+    "rho in own CTAs": {"NLINV_RHO_SPREAD": "0"},
+    "persistent frame kernel": {"NLINV_FRAME": "1", "NLINV_DATAFLOW": "0"},
+    "frame kernel, dataflow": {"NLINV_FRAME": "1", "NLINV_DATAFLOW": "1"},
+}
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
+@pytest.mark.parametrize("ng,J,spokes,turns,K,L", [(64, 6, 11, 1, 2, 6), (384, 12, 15, 5, 1, 4)])
+def test_execution_variants_match_oracle(variant, ng, J, spokes, turns, K, L):
+    """Every execution path of the library (read from the environment at plan creation) gives
+    the oracle's frame: the fused cooperative passes, the unfused multi-kernel path used for
+    world > 1, and the persistent frame kernel (barrier and dataflow schedules)."""
+    B = _B()
+    old = {k: os.environ.get(k) for k in VARIANTS[variant]}
+    os.environ.update(VARIANTS[variant])
+    try:
+        y, mask = _frame(ng, J, spokes, turns)
+        plan = B.Plan(ng, J, mask)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    x, img = plan.reconstruct(dev(y), None, K, L)
+    xo, io, hist = _oracle_recon(y, mask, K, L)
+    assert rel(host(img), io) < 1e-4
+    assert rel(host(x), xo) < 1e-4
+    assert np.allclose(plan.stats()["residual"], hist, rtol=1e-4)
+    plan.close()
