@@ -693,11 +693,13 @@ __device__ __forceinline__ void row_task(const RowArgs& a, int pair0, const floa
       for (int i = t; i < n; i += T) a.rho_omega[(size_t)yy * n + i] = a.xrho[(size_t)row * L + q + i];
   }
   float2 v[E];
+  // Unconditional loads: an inactive group (tail of the last CTA) transforms a valid row it never
+  // stores. A per-element "if (active)" makes the compiler put each load and its first use in one
+  // branch region, which serialises the E load latencies.
+  {
+    const float2* src = a.in + (active ? j * H + (size_t)yy * L : 0);
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int xi = S::in_idx(t, e);
-    v[e] = make_float2(0.f, 0.f);
-    if (active) v[e] = cneg_if(a.in[j * H + (size_t)yy * L + xi], xi & 1);
+    for (int e = 0; e < E; ++e) v[e] = cneg_if(src[S::in_idx(t, e)], S::in_idx(t, e) & 1);
   }
   if (tw_async) tw_wait();
   fft<L, +1>(v, t, tw, buf, SyncWarp{});
@@ -823,11 +825,10 @@ __device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, int jlo, i
     const int j = j0 + g;
     const bool active = j < jhi;
     float2 v[E], cv[E / 2];
+    {  // unconditional loads (see row_task); an inactive group's result is masked below
+      const float2* src = a.in + (size_t)(active ? j : jlo) * H + (size_t)yy * L;
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int xi = S::in_idx(t, e);
-      v[e] = make_float2(0.f, 0.f);
-      if (active) v[e] = cneg_if(a.in[j * H + (size_t)yy * L + xi], xi & 1);
+      for (int e = 0; e < E; ++e) v[e] = cneg_if(src[S::in_idx(t, e)], S::in_idx(t, e) & 1);
     }
     {
       int u = 0;
@@ -1594,10 +1595,7 @@ __global__ void __launch_bounds__(256) fft_rows_tw_kernel(const float2* __restri
   float2 v[E];
   const bool active = rowi < nrows;
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int xi = S::in_idx(t, e);
-    v[e] = active ? cneg_if(in[rowi * L + xi], xi & 1) : make_float2(0.f, 0.f);
-  }
+  for (int e = 0; e < E; ++e) v[e] = cneg_if(in[(active ? rowi * L : 0) + S::in_idx(t, e)], S::in_idx(t, e) & 1);
   fft<L, DIR>(v, t, tw, buf, SyncWarp{});
   if (active) {
 #pragma unroll
