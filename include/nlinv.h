@@ -176,6 +176,21 @@ nlinv_status nlinv_stream_frame(nlinv_plan plan, const nlinv_c32* frame_host, co
                                 int newton_steps, int cg_iters, nlinv_c32* image_host, void* stream);
 nlinv_status nlinv_stream_reset(nlinv_plan plan);
 
+/* The sampled cells of the plan's current P_k as ascending linear indices y*ng + x (
+ * integer-exact, computed on the device by stream compaction). idx_host: host int[cap] or NULL
+ * (count only); *nnz_host receives the count. ERR_SIZE if cap < count. Synchronises `stream`. */
+nlinv_status nlinv_mask_indices(nlinv_plan plan, int* idx_host, int cap, int* nnz_host, void* stream);
+
+/* Streaming entry with a COMPACT frame: samples_host holds, for each local coil, the gridded
+ * k-space values at the sampled cells of this frame's P_k in ascending linear-index order
+ * ([count][nnz], nnz = number of sampled cells, as nlinv_mask_indices returns). This is the same
+ * gridded frame as nlinv_stream_frame without its zeros (after gridding every operation
+ * is on the grid; only P_k . y enters the method, R16), ~3.7 % of the bytes at C2. mask_host:
+ * this frame's P_k (host uint8 [ng][ng]) or NULL to keep the current one. Synchronises. */
+nlinv_status nlinv_stream_frame_compact(nlinv_plan plan, const nlinv_c32* samples_host, int nnz,
+                                        const uint8_t* mask_host, int newton_steps, int cg_iters,
+                                        nlinv_c32* image_host, void* stream);
+
 /* Per-kernel timing: with profiling on, reconstruct/operator calls run without CUDA graphs and
  * bracket every kernel with CUDA events on its stream. nlinv_plan_profile_json synchronises and
  * writes {"kernel": [launches, total_ms], ...} into buf (ERR_SIZE if len is too small), then

@@ -77,6 +77,10 @@ struct nlinv_plan_s {
   unsigned* counter = nullptr;
   // host e2e staging (device side)
   float2 *h_frame = nullptr, *h_x = nullptr, *h_img = nullptr;
+  // sampled-cell index list of P_k (nlinv_mask_indices, compact ingest)
+  int *midx = nullptr, *mcount = nullptr, *mnnz = nullptr;
+  float2* h_samples = nullptr;
+  long long mnnz_host = -1;  // count of midx; -1 = index list stale (P_k changed)
   // graph cache
   GraphKey gkey;
   cudaGraphExec_t gexec = nullptr;
@@ -235,7 +239,7 @@ static void plan_free(nlinv_plan pl) {
   void* ptrs[] = {pl->tw, pl->winv, pl->mask, pl->xref, pl->dx, pl->r, pl->p, pl->Ap, pl->tA, pl->tB,
                   pl->c_omega, pl->rho_omega, pl->S_all, pl->S, pl->S_sum, pl->rss_all, pl->rss, pl->rss_sum,
                   pl->fred, pl->fbar, pl->fdone, pl->ftred, pl->tstamp, pl->kbar, pl->kpart, pl->scal, pl->partials,
-                  pl->counter, pl->h_frame, pl->h_x, pl->h_img};
+                  pl->counter, pl->h_frame, pl->h_x, pl->h_img, pl->midx, pl->mcount, pl->mnnz, pl->h_samples};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
@@ -396,12 +400,14 @@ extern "C" nlinv_status nlinv_plan_set_mask(nlinv_plan pl, const uint8_t* mask_h
   std::vector<uint8_t> m8(pl->N);
   for (size_t i = 0; i < pl->N; ++i) m8[i] = mask_host[i] ? 1 : 0;
   CU(cudaMemcpy(pl->mask, m8.data(), pl->N, cudaMemcpyHostToDevice));
+  pl->mnnz_host = -1;
   return NLINV_OK;
 }
 
 extern "C" nlinv_status nlinv_plan_set_mask_device(nlinv_plan pl, const uint8_t* mask_dev, void* stream) {
   if (!pl || !mask_dev) return fail(pl, NLINV_ERR_ARG, "NULL argument");
   CU(cudaMemcpyAsync(pl->mask, mask_dev, pl->N, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  pl->mnnz_host = -1;
   return NLINV_OK;
 }
 
@@ -1003,7 +1009,10 @@ extern "C" nlinv_status nlinv_stream_frame(nlinv_plan pl, const nlinv_c32* frame
     CU(cudaMalloc((void**)&pl->h_img, sizeof(float2) * pl->Q));
   }
   CU(cudaMemcpyAsync(pl->h_frame, frame_host, sizeof(float2) * N * pl->J, cudaMemcpyHostToDevice, s));
-  if (mask_host) CU(cudaMemcpyAsync(pl->mask, mask_host, N, cudaMemcpyHostToDevice, s));
+  if (mask_host) {
+    CU(cudaMemcpyAsync(pl->mask, mask_host, N, cudaMemcpyHostToDevice, s));
+    pl->mnnz_host = -1;
+  }
   nlinv_status st = nlinv_reconstruct(pl, (const nlinv_c32*)pl->h_frame,
                                       pl->stream_started ? (const nlinv_c32*)pl->h_x : nullptr, newton_steps,
                                       cg_iters, (nlinv_c32*)pl->h_x, image_host ? (nlinv_c32*)pl->h_img : nullptr,
@@ -1090,5 +1099,76 @@ extern "C" nlinv_status nlinv_plan_trace(nlinv_plan pl, int col_mode, unsigned l
   CU(cudaDeviceSynchronize());
   CU(cudaMemcpy(out, pl->trace, sizeof(unsigned long long) * (cap < 8 * 8192 ? cap : 8 * 8192), cudaMemcpyDeviceToHost));
   pl->trace_mode = -1;
+  return NLINV_OK;
+}
+
+// ------------------------------------------------------------------ P_k index list and compact ingest
+static nlinv_status ensure_index_buffers(nlinv_plan pl) {
+  if (!pl->midx) {
+    CU(cudaMalloc((void**)&pl->midx, sizeof(int) * pl->N));
+    CU(cudaMalloc((void**)&pl->mcount, sizeof(int) * mask_count_blocks((int)pl->N)));
+    CU(cudaMalloc((void**)&pl->mnnz, sizeof(int)));
+  }
+  return NLINV_OK;
+}
+
+extern "C" nlinv_status nlinv_mask_indices(nlinv_plan pl, int* idx_host, int cap, int* nnz_host, void* stream) {
+  if (!pl || !nnz_host) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  nlinv_status st = ensure_index_buffers(pl);
+  if (st != NLINV_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  CU(launch_mask_compact(pl->mask, (int)pl->N, pl->mcount, pl->midx, pl->mnnz, s));
+  pl->launches += 2;
+  int nnz = 0;
+  CU(cudaMemcpyAsync(&nnz, pl->mnnz, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  *nnz_host = nnz;
+  pl->mnnz_host = nnz;
+  if (idx_host) {
+    if (cap < nnz) return fail(pl, NLINV_ERR_SIZE, "idx buffer smaller than nnz");
+    CU(cudaMemcpy(idx_host, pl->midx, sizeof(int) * nnz, cudaMemcpyDeviceToHost));
+  }
+  return NLINV_OK;
+}
+
+extern "C" nlinv_status nlinv_stream_frame_compact(nlinv_plan pl, const nlinv_c32* samples_host, int nnz,
+                                                   const uint8_t* mask_host, int newton_steps, int cg_iters,
+                                                   nlinv_c32* image_host, void* stream) {
+  if (!pl || !samples_host || nnz < 0 || (size_t)nnz > pl->N) return fail(pl, NLINV_ERR_ARG, "bad argument");
+  const size_t N = pl->N, tot = N * (1 + pl->J);
+  cudaStream_t s = (cudaStream_t)stream;
+  nlinv_status st = ensure_index_buffers(pl);
+  if (st != NLINV_OK) return st;
+  if (!pl->h_frame) {
+    CU(cudaMalloc((void**)&pl->h_frame, sizeof(float2) * N * pl->J));
+    CU(cudaMemset(pl->h_frame, 0, sizeof(float2) * N * pl->J));
+    CU(cudaMalloc((void**)&pl->h_x, sizeof(float2) * tot));
+    CU(cudaMalloc((void**)&pl->h_img, sizeof(float2) * pl->Q));
+  }
+  if (!pl->h_samples) CU(cudaMalloc((void**)&pl->h_samples, sizeof(float2) * N * pl->J));
+  if (mask_host) {
+    long long cnt = 0;
+    for (size_t i = 0; i < N; ++i) cnt += mask_host[i] ? 1 : 0;
+    CU(cudaMemcpyAsync(pl->mask, mask_host, N, cudaMemcpyHostToDevice, s));
+    CU(launch_mask_compact(pl->mask, (int)N, pl->mcount, pl->midx, pl->mnnz, s));
+    pl->launches += 2;
+    pl->mnnz_host = cnt;
+  } else if (pl->mnnz_host < 0) {
+    int cnt = 0;
+    st = nlinv_mask_indices(pl, nullptr, 0, &cnt, stream);
+    if (st != NLINV_OK) return st;
+    pl->mnnz_host = cnt;
+  }
+  if ((long long)nnz != pl->mnnz_host) return fail(pl, NLINV_ERR_SIZE, "nnz differs from the sampled-cell count of P_k");
+  CU(cudaMemcpyAsync(pl->h_samples, samples_host, sizeof(float2) * (size_t)nnz * pl->J, cudaMemcpyHostToDevice, s));
+  CU(launch_scatter_samples(pl->h_samples, pl->midx, pl->mnnz, nnz, pl->J, N, pl->h_frame, s));
+  pl->launches += 1;
+  st = nlinv_reconstruct(pl, (const nlinv_c32*)pl->h_frame, pl->stream_started ? (const nlinv_c32*)pl->h_x : nullptr,
+                         newton_steps, cg_iters, (nlinv_c32*)pl->h_x, image_host ? (nlinv_c32*)pl->h_img : nullptr,
+                         stream);
+  if (st != NLINV_OK) return st;
+  pl->stream_started = true;
+  if (image_host) CU(cudaMemcpyAsync(image_host, pl->h_img, sizeof(float2) * pl->Q, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
   return NLINV_OK;
 }

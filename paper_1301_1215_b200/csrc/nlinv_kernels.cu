@@ -162,6 +162,84 @@ __global__ void init_x_kernel(float2* x, long long nrho, long long ntot) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ntot; i += (long long)gridDim.x * blockDim.x)
     x[i] = make_float2(i < nrho ? 1.0f : 0.0f, 0.0f);
 }
+// ------------------------------------------------------------------ P_k -> sorted index list (a0)
+// Stream compaction of the sampling mask into ascending linear indices (integer-exact):
+// pass 1 counts the sampled cells of each 4096-cell chunk, pass 2 gives every chunk its offset
+// (ordered prefix of the counts) and writes its indices in order with warp ballots.
+constexpr int kMaskChunk = 4096;
+__global__ void __launch_bounds__(256) mask_count_kernel(const uint8_t* __restrict__ mask, int N, int* counts) {
+  __shared__ int red[8];
+  pdl_wait();
+  const int base = blockIdx.x * kMaskChunk;
+  int c = 0;
+  for (int i = threadIdx.x; i < kMaskChunk; i += 256)
+    if (base + i < N && mask[base + i]) ++c;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    counts[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) mask_scatter_kernel(const uint8_t* __restrict__ mask, int N,
+                                                           const int* __restrict__ counts, int* idx, int* nnz) {
+  __shared__ int s_off, s_warp[8];
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int b = 0; b < (int)blockIdx.x; ++b) o += counts[b];
+    s_off = o;
+    if (blockIdx.x == gridDim.x - 1) *nnz = o + counts[blockIdx.x];
+  }
+  __syncthreads();
+  const int base = blockIdx.x * kMaskChunk;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int off = s_off;
+  for (int i0 = 0; i0 < kMaskChunk; i0 += 256) {
+    const int i = base + i0 + threadIdx.x;
+    const bool m = (i < N) && mask[i];
+    const unsigned bal = __ballot_sync(0xffffffffu, m);
+    if (lane == 0) s_warp[w] = __popc(bal);
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int ww = 0; ww < 8; ++ww) {
+      if (ww < w) before += s_warp[ww];
+      tot += s_warp[ww];
+    }
+    if (m) idx[off + before + __popc(bal & ((1u << lane) - 1u))] = i;
+    off += tot;
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_mask_compact(const uint8_t* mask, int N, int* counts, int* idx, int* nnz, cudaStream_t s) {
+  const int nb = (N + kMaskChunk - 1) / kMaskChunk;
+  cudaError_t e = launch_k(mask_count_kernel, dim3(nb), dim3(256), 0, s, mask, N, counts);
+  if (e != cudaSuccess) return e;
+  return launch_k(mask_scatter_kernel, dim3(nb), dim3(256), 0, s, mask, N, (const int*)counts, idx, nnz);
+}
+int mask_count_blocks(int N) { return (N + kMaskChunk - 1) / kMaskChunk; }
+
+// compact frame ingest (a1): y_j[idx[s]] = samples_j[s]; cells off P_k are never read
+__global__ void scatter_samples_kernel(const float2* __restrict__ samples, const int* __restrict__ idx,
+                                       const int* __restrict__ nnz_p, int nnz_cap, int J, size_t N, float2* y) {
+  pdl_wait();
+  const int nnz = *nnz_p;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)J * nnz;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i / nnz), s = (int)(i % nnz);
+    y[(size_t)j * N + idx[s]] = samples[(size_t)j * nnz_cap + s];
+  }
+}
+cudaError_t launch_scatter_samples(const float2* samples, const int* idx, const int* nnz, int nnz_cap, int J,
+                                   size_t N, float2* y, cudaStream_t s) {
+  return launch_k(scatter_samples_kernel, dim3(148 * 4), dim3(256), 0, s, samples, idx, nnz, nnz_cap, J, N, y);
+}
+
 cudaError_t launch_init_x(float2* x, long long nrho, long long ntot, cudaStream_t s) {
   return launch_k(init_x_kernel, dim3(vec_grid(ntot)), dim3(kVecThreads), 0, s, x, nrho, ntot);
 }

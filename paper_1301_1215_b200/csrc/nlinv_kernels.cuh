@@ -159,6 +159,10 @@ int col_tiles(int ng);  // column-kernel CTAs per coil
 cudaError_t launch_init_x(float2* x, long long nrho, long long ntot, cudaStream_t s);
 cudaError_t launch_frame(int ng, const FrameArgs& f, cudaStream_t s);
 bool frame_supported(int ng);
+cudaError_t launch_mask_compact(const uint8_t* mask, int N, int* counts, int* idx, int* nnz, cudaStream_t s);
+int mask_count_blocks(int N);
+cudaError_t launch_scatter_samples(const float2* samples, const int* idx, const int* nnz, int nnz_cap, int J,
+                                   size_t N, float2* y, cudaStream_t s);
 bool col_fusable(int ng, int J);
 cudaError_t launch_coil_sum(int ng, const float2* S_all, int J, float2* S, cudaStream_t s);
 cudaError_t launch_rss_sum(int ng, const float* rss_all, int J, float* rss, cudaStream_t s);

@@ -68,6 +68,8 @@ _SIGS = {
     "nlinv_plan_launch_count": (c_ll, [c_void_p]),
     "nlinv_stream_frame": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]),
     "nlinv_stream_reset": (c_int, [c_void_p]),
+    "nlinv_mask_indices": (c_int, [c_void_p, c_void_p, c_int, ctypes.POINTER(c_int), c_void_p]),
+    "nlinv_stream_frame_compact": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_int, c_int, c_void_p, c_void_p]),
     "nlinv_plan_set_profiling": (c_int, [c_void_p, c_int]),
     "nlinv_plan_phase_times": (c_int, [c_void_p, c_int, c_void_p, c_int, ctypes.POINTER(c_int)]),
     "nlinv_plan_trace": (c_int, [c_void_p, c_int, c_void_p, c_int]),
@@ -257,6 +259,37 @@ class Plan:
             ip = ctypes.c_void_p(image_out.data_ptr())
         _check(_lib.nlinv_stream_frame(self._h, ctypes.c_void_p(frame.data_ptr()), mp, int(newton_steps),
                                        int(cg_iters), ip, _stream_ptr(stream)), self._h)
+        return image_out
+
+    def mask_indices(self, stream=None) -> np.ndarray:
+        """Ascending linear indices of the plan's current P_k (computed on the device)."""
+        nnz = c_int()
+        _check(_lib.nlinv_mask_indices(self._h, None, 0, ctypes.byref(nnz), _stream_ptr(stream)), self._h)
+        out = np.zeros(max(nnz.value, 1), dtype=np.int32)
+        _check(_lib.nlinv_mask_indices(self._h, out.ctypes.data, out.size, ctypes.byref(nnz), _stream_ptr(stream)),
+               self._h)
+        return out[:nnz.value]
+
+    def stream_frame_compact(self, samples, mask=None, newton_steps=7, cg_iters=10, image_out=None, stream=None):
+        """Real-time entry with a compact frame: host complex64 [count, nnz] samples at the sampled
+        cells (ascending index order), optional host uint8 mask of this frame, host image out."""
+        import torch
+        if samples.is_cuda or samples.dtype != torch.complex64 or samples.dim() != 2 \
+                or samples.shape[0] != self.count or not samples.is_contiguous():
+            raise ValueError(f"samples must be a contiguous CPU complex64 tensor [{self.count}, nnz]")
+        mp = None
+        if mask is not None:
+            if not (isinstance(mask, torch.Tensor) and not mask.is_cuda and mask.dtype == torch.uint8
+                    and tuple(mask.shape) == (self.ng, self.ng) and mask.is_contiguous()):
+                raise ValueError("mask must be a contiguous CPU uint8 tensor [ng, ng]")
+            mp = ctypes.c_void_p(mask.data_ptr())
+        ip = None
+        if image_out is not None:
+            if image_out.is_cuda or image_out.dtype != torch.complex64 or tuple(image_out.shape) != self.image_shape:
+                raise ValueError("image_out must be a CPU complex64 tensor [n, n]")
+            ip = ctypes.c_void_p(image_out.data_ptr())
+        _check(_lib.nlinv_stream_frame_compact(self._h, ctypes.c_void_p(samples.data_ptr()), int(samples.shape[1]), mp,
+                                               int(newton_steps), int(cg_iters), ip, _stream_ptr(stream)), self._h)
         return image_out
 
     def stream_reset(self):

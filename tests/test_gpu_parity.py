@@ -232,6 +232,47 @@ def test_reconstruct_host_e2e_matches_device():
     plan.close()
 
 
+@pytest.mark.parametrize("ng", [16, 48, 96, 384, 1024])
+def test_mask_indices_bitexact(ng):
+    """P_k -> ascending sampled-cell indices: integer work, bit-exact vs flatnonzero,
+    on the radial pattern, a random pattern, the empty and the full pattern (ragged last chunk for
+    ng = 48, 96)."""
+    B = _B()
+    rnd = (synth.splitmix64_uniform(ng, ng * ng) < 0.3).astype(np.uint8).reshape(ng, ng)
+    masks = [O.radial_mask(ng, 15, 5, 2), rnd, np.zeros((ng, ng), np.uint8), np.ones((ng, ng), np.uint8)]
+    plan = B.Plan(ng, 1, masks[0])
+    for m in masks:
+        plan.set_mask(m)
+        got = plan.mask_indices()
+        assert got.dtype == np.int32 and np.array_equal(got, np.flatnonzero(m))
+    plan.close()
+
+
+def test_stream_frame_compact_matches_full():
+    """Compact ingest (only the P_k samples cross PCIe) == full-grid ingest, bit for bit, over a
+    3-frame stream with a changing P_k; the sample count is validated against P_k."""
+    B = _B()
+    ng, J, K, L = 64, 4, 2, 4
+    pf = B.Plan(ng, J, O.radial_mask(ng, 11, 3, 0))
+    pc = B.Plan(ng, J, O.radial_mask(ng, 11, 3, 0))
+    for f, mf in ((0, 0), (1, 1), (2, None)):  # frame 2 keeps frame 1's P_k (mask=None)
+        y, _ = _frame(ng, J, 11, 3, f)
+        m = O.radial_mask(ng, 11, 3, 1 if mf is None else mf)
+        mt = None if mf is None else torch.from_numpy(m)
+        idx = np.flatnonzero(m)
+        samples = torch.from_numpy(np.ascontiguousarray(y.reshape(J, -1)[:, idx]))
+        i_full = torch.empty(pf.image_shape, dtype=torch.complex64)
+        i_comp = torch.empty(pc.image_shape, dtype=torch.complex64)
+        pf.stream_frame(torch.from_numpy(y), mt, K, L, i_full)
+        pc.stream_frame_compact(samples, mt, K, L, i_comp)
+        assert torch.equal(i_full, i_comp)
+    with pytest.raises(B.NlinvError) as e:
+        pc.stream_frame_compact(samples[:, :-1].contiguous(), None, K, L, i_comp)
+    assert e.value.status == 2  # NLINV_ERR_SIZE
+    pf.close()
+    pc.close()
+
+
 def test_reconstruct_c2_newton_step_full_size():
     """BASELINE config 2 shape (12 coils, 384^2, 15 spokes, T=5) in bench's launch configuration,
     one Newton step x 10 CG against the oracle."""
