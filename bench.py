@@ -59,12 +59,16 @@ def algo_bytes(name: str, ng: int, Jl: int, L: int = CG) -> float:
         # K5 fused with the CG residual update (cooperative): T4, p, w^-1, r in, r out per coil;
         # rho stripe: S, p_rho in, Ap_rho out and back in, r_rho in and out
         "col_fft_w_normal_upd": 32 * Jl * N + 4 * N + 50 * N,
-        # ... + beta and K1 of the next iteration on the same tile (p, dx in; p, dx, T1 out)
-        "col_k5_cg_k1": 72 * Jl * N + 4 * N + 74 * N,
-        # ... last iteration: + the Newton update x += dx + gamma p (p, dx, x in; x out)
-        "col_k5_newton": 48 * Jl * N + 4 * N + 50 * N,
+        # ... + beta and K1 of the next iteration on the same tile. Compulsory operands only, each
+        # counted once per launch: per coil T4 (Omega rows) 4, p 8, r 8+8, dx 8+8, p out 8, T1 out 4;
+        # w^-1 once; rho block: coil-sum plane 2, p 8, r 8+8, dx 8+8, p out 8 (the A p_rho round
+        # trip and the second p read are implementation re-reads, not counted)
+        "col_k5_cg_k1": 56 * Jl * N + 4 * N + 50 * N,
+        # ... last iteration: + the Newton update x += dx + gamma p (T4, p, dx, x in; x out)
+        "col_k5_newton": 36 * Jl * N + 4 * N + 34 * N,
         # Newton rhs + K1 of CG iteration 0 (T1 out)
-        "col_rhs_k1": 4 * Jl * N + 8 * Jl * N + 8 * Jl * N + 4 * N + 16 * Jl * N + 34 * N + 4 * Jl * N,
+        # T in 4, chat 8, chat_ref 8, b out once 8 (r = p = b), T1 out 4; w^-1; rho block
+        "col_rhs_k1": 32 * Jl * N + 4 * N + 34 * N,
         "r_update": 24 * N * (Jl + 1),                       # r, Ap in; r out
         "newton_update": 32 * N * (Jl + 1),                  # p, dx, x in; x out
         "col_ifft_w": 8 * Jl * N + 4 * N + 4 * Jl * N,
