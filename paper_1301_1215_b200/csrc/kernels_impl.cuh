@@ -29,6 +29,7 @@ struct ColGeo {
   static constexpr int CW = (L % c0 == 0) ? c0 : ((L % 16 == 0 && c0 >= 16) ? 16 : 8);
   static constexpr int THREADS = CW * T;
   static constexpr size_t SMEM = sizeof(float2) * (size_t)L * (CW + 1) + 64 * sizeof(double);
+  static constexpr size_t SMEM_PF = SMEM + 64 * sizeof(double) + sizeof(float2) * (size_t)L * CW;   // k5cg_kernel
 };
 
 
@@ -45,9 +46,14 @@ struct ColBuf {
   int c;
   __device__ __forceinline__ float2& operator()(int i) const { return s[i * CW + c]; }
 };
+// Row exchange buffer with an XOR swizzle: slot i lives at i ^ ((i >> 4) & 7). The first Stockham
+// pass stores at stride R (8 at L = 384), which unswizzled puts the 16 lanes of a transform on two
+// bank pairs (16-way conflict); the swizzle only permutes within aligned 16-slot blocks, so the
+// reads "t + 16 m + const" stay conflict-free and cost one XOR with a compile-time key.
+__host__ __device__ constexpr int rsw(int i) { return i ^ ((i >> 4) & 7); }
 struct RowBuf {
   float2* s;
-  __device__ __forceinline__ float2& operator()(int i) const { return s[i]; }
+  __device__ __forceinline__ float2& operator()(int i) const { return s[rsw(i)]; }
 };
 
 __device__ __forceinline__ float sgn_of(int i) { return (i & 1) ? -1.0f : 1.0f; }
@@ -170,6 +176,30 @@ __device__ __forceinline__ void tw_copy_async(float2* tw_s, const float2* tw_g, 
 __device__ __forceinline__ void tw_wait() {
   asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
+}
+// ... while one later commit group (a tile prefetch) may stay in flight
+__device__ __forceinline__ void tw_wait_keep1() {
+  asm volatile("cp.async.wait_group 1;\n" ::);
+  __syncthreads();
+}
+
+__device__ __forceinline__ void prefetch_wait() {
+  asm volatile("cp.async.wait_all;\n" ::);
+  __syncthreads();
+}
+
+// Column-tile prefetch: rows 0..L-1, columns x0..x0+CW-1 of one [L][L] c64 image into shared
+// memory laid out [row][CW] (the ColBuf layout: thread (t, c) later reads its rows k at
+// dst[k * CW + c]); 16-byte cp.async.cg (L2 only), one commit group.
+template <int L, int CW>
+__device__ __forceinline__ void tile_prefetch(float2* dst, const float2* img, int x0) {
+  constexpr int CPR = CW / 2;  // 16-byte chunks per row
+  for (int i = threadIdx.x; i < L * CPR; i += blockDim.x) {
+    const int row = i / CPR, c2 = i - row * CPR;
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + row * CW + 2 * c2);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(img + (size_t)row * L + x0 + 2 * c2));
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
 }
 
 // debug timeline of one CTA (globaltimer ns), compiled in with -DNLV_TRACE
@@ -456,6 +486,7 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
         const unsigned nb = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
         double* sred = reinterpret_cast<double*>(xb);   // the exchange buffer is free here
         __syncthreads();
+        trace_stamp(a.trace, 7);
         const double pr = block_sum(acc_rho, sred);
         const double pc = block_sum(acc, sred);
         if (threadIdx.x == 0) {
@@ -463,6 +494,7 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
           a.fpart[2 * bid + 1] = pc;
         }
         grid_barrier_n(a.bar_count, a.bar_gen, nb);
+        trace_stamp(a.trace, 3);
         double tr = 0.0, tc = 0.0;
         for (unsigned b = threadIdx.x; b < nb; b += blockDim.x) {
           tr += __ldcg(a.fpart + 2 * b);
@@ -540,6 +572,7 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
               a.fpart[2 * nb + 2 * bid + 1] = rr_c;
             }
             grid_barrier_n(a.bar_count, a.bar_gen, nb);
+            trace_stamp(a.trace, 4);
             double ur = 0.0, uc = 0.0;
             for (unsigned b2 = threadIdx.x; b2 < nb; b2 += blockDim.x) {
               ur += __ldcg(a.fpart + 2 * nb + 2 * b2);
@@ -666,6 +699,264 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColAr
       grid_finish<2>(vv, a.partials, a.counter, a.scal_w, sl, red);
     }
   }
+  trace_stamp(a.trace, 6);
+}
+
+
+// ------------------------------------------------------------------ fused K5 + CG + K1, one grid barrier
+// One CG iteration's tail (P:233 CG) as one cooperative pass with a SINGLE grid
+// barrier: K5 (column FFT -> A p = w^-1 . + alpha p) and, before the barrier, the block dots
+// <p,Ap>, <r,r>, <r,Ap>, <Ap,Ap> (rho and chat parts). After the barrier every CTA forms, in the
+// same fixed order,
+//   gamma_i = <r_i,r_i> / <p_i,Ap_i>,   <r_i,r_i> of the stored r_i, computed in this pass
+//   <r_{i+1},r_{i+1}> = <r_i,r_i> - 2 gamma_i Re<r_i,Ap_i> + gamma_i^2 <Ap_i,Ap_i>   (R19)
+//   beta_i = <r_{i+1},r_{i+1}> / <r_i,r_i>
+// and runs r -= gamma Ap, dx += gamma p, p = r + beta p and K1 of iteration i+1 (w^-1 p -> column
+// IFFT -> T1) on its tile; the last iteration does the Newton update x += dx + gamma p instead.
+// r (or dx) is prefetched into shared memory while the K5 transform runs; p is parked in the
+// exchange buffer. The textbook form needs a second barrier for <r_{i+1}, r_{i+1}> (R19). <r_i,r_i>
+// must be the directly computed one: feeding the expanded value back into the next expansion
+// accumulates its absolute error and ruins late iterations (measured in an fp32 model: 5e-2 on
+// the C1 image vs 6e-5 with the direct <r_i,r_i>).
+template <int L>
+__device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, float2* xb, float2* pf, double* red) {
+  using C = Cfg<L>;
+  using S = Sched<L>;
+  constexpr int T = C::T, E = C::E, CW = ColGeo<L>::CW;
+  constexpr int n = L / 2, q = L / 4;
+  constexpr size_t N = (size_t)L * L, H = (size_t)n * L, Qs = (size_t)n * n;
+  constexpr float invL = 1.0f / (float)L;
+  constexpr int NV = 8;   // pAp, rAp, ApAp, rr; each (rho, chat)
+  const int tid = threadIdx.x, c = tid % CW, t = tid / CW;
+  const int tile = blockIdx.x, j = blockIdx.y;
+  const int x = tile * CW + c;
+  const bool last = a.last_iter != 0, hasdx = a.iter > 0;
+  const unsigned nb = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
+  ColBuf<CW> buf{xb, c};
+
+  bool pf_on = false;
+  if (!last) {
+    tile_prefetch<L, CW>(pf, a.r + j * N, tile * CW);
+    pf_on = true;
+  } else if (hasdx) {
+    tile_prefetch<L, CW>(pf, a.dx + j * N, tile * CW);
+    pf_on = true;
+  }
+
+  // prologue: T4 (Omega rows only; the others are zero)
+  float2 v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    if (in_is_omega<L>(e)) {
+      const int yr = S::in_idx(t, e);
+      v[e] = cneg_if(a.in[j * H + (size_t)(yr - q) * L + x], yr & 1);
+    } else {
+      v[e] = make_float2(0.f, 0.f);
+    }
+  }
+
+  // rho block stripe of this tile: A p_rho = M sum_s S_s + alpha p_rho (replicated rho)
+  double d[NV] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  constexpr int NTILE = L / CW;
+  const int nstripe = a.J * NTILE, stripe = j * NTILE + tile;
+  const size_t chunk = (N + nstripe - 1) / nstripe;
+  const size_t lo = (size_t)stripe * chunk, hi = (lo + chunk < N) ? lo + chunk : N;
+  for (size_t i = lo + tid; i < hi; i += blockDim.x) {
+    const int y = (int)(i / L), xx = (int)(i % L);
+    float2 sv = make_float2(0.f, 0.f);
+    if (xx >= q && xx < q + n && y >= q && y < q + n) {
+      const size_t o = (size_t)(y - q) * n + (xx - q);
+      for (int sp = 0; sp < a.nS; ++sp) sv = cadd(sv, a.S[sp * Qs + o]);
+    }
+    const float2 pv = a.rho_a[i];
+    const float2 o = make_float2(fmaf(a.alpha, pv.x, sv.x), fmaf(a.alpha, pv.y, sv.y));
+    a.rho_out[i] = o;
+    d[0] += (double)pv.x * o.x + (double)pv.y * o.y;
+    if (!last) {
+      const float2 rv = a.rho_r[i];
+      d[2] += (double)rv.x * o.x + (double)rv.y * o.y;
+      d[4] += (double)o.x * o.x + (double)o.y * o.y;
+      d[6] += (double)rv.x * rv.x + (double)rv.y * rv.y;
+    }
+  }
+
+  if (pf_on) tw_wait_keep1();
+  else tw_wait();
+  trace_stamp(a.trace, 1);
+  fft<L, -1>(v, t, tw, buf, SyncBlock{});
+  trace_stamp(a.trace, 2);
+  if (pf_on) prefetch_wait();   // the r / dx tile is complete (all threads' copies)
+
+  // epilogue: A p_chat = w^-1 (-1)^k . + alpha p; p parked in the (now free) exchange buffer
+  {
+    constexpr int CH = 8;
+#pragma unroll
+    for (int e0 = 0; e0 < E; e0 += CH) {
+      float wv[CH];
+      float2 pv[CH];
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const size_t i = (size_t)S::out_idx(t, e0 + u) * L + x;
+        wv[u] = a.winv[i];
+        pv[u] = a.p[j * N + i];
+      }
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const int k = S::out_idx(t, e0 + u);
+        const float2 val = cscale(v[e0 + u], wv[u] * sgn_of(k));
+        const float2 o = make_float2(fmaf(a.alpha, pv[u].x, val.x), fmaf(a.alpha, pv[u].y, val.y));
+        v[e0 + u] = o;
+        buf(k) = pv[u];
+        d[1] += (double)pv[u].x * o.x + (double)pv[u].y * o.y;
+        if (!last) {
+          const float2 rv = pf[k * CW + c];
+          d[3] += (double)rv.x * o.x + (double)rv.y * o.y;
+          d[5] += (double)o.x * o.x + (double)o.y * o.y;
+          d[7] += (double)rv.x * rv.x + (double)rv.y * rv.y;
+        }
+      }
+    }
+  }
+  trace_stamp(a.trace, 7);
+
+  // block partials (warp trees, then warps in index order) -> fpart[k][bid]; grid barrier
+  {
+    const int w = tid >> 5, lane = tid & 31, nw = (int)(blockDim.x >> 5);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double vk = d[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) vk += __shfl_xor_sync(0xffffffffu, vk, o);
+      if (lane == 0) red[8 + w * NV + k] = vk;
+    }
+    __syncthreads();
+    if (tid < NV) {
+      double sk = 0.0;
+      for (int ww = 0; ww < nw; ++ww) sk += red[8 + ww * NV + tid];
+      a.fpart[tid * nb + bid] = sk;
+    }
+    grid_barrier_n(a.bar_count, a.bar_gen, nb);
+    trace_stamp(a.trace, 3);
+    // totals: warp w sums value k = w (+ nw ...) over all CTAs in a fixed order -> identical in every CTA
+    for (int k = w; k < NV; k += nw) {
+      double sk = 0.0;
+      for (unsigned b = lane; b < nb; b += 32) sk += __ldcg(a.fpart + k * nb + b);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sk += __shfl_xor_sync(0xffffffffu, sk, o);
+      if (lane == 0) red[k] = sk;
+    }
+    __syncthreads();
+  }
+  // <r_i, r_i>: computed in this pass; the last iteration (no r read) takes the previous pass's value
+  const double rr_r = last ? a.scal[SC_RR_RHO + a.iter] : red[6];
+  const double rr_c = last ? a.scal[SC_RR_CHAT + a.iter] : red[7];
+  const double rr = rr_r + rr_c;
+  const double pap = red[0] + red[1];
+  const float gamma = (rr != 0.0) ? (float)(rr / pap) : 0.0f;
+  float beta = 0.0f;
+  if (!last) {
+    const double g = (double)gamma;
+    const double nr = fmax(rr_r - 2.0 * g * red[2] + g * g * red[4], 0.0);
+    const double nc = fmax(rr_c - 2.0 * g * red[3] + g * g * red[5], 0.0);
+    beta = (rr != 0.0) ? (float)((nr + nc) / rr) : 0.0f;
+    if (bid == 0 && tid == 0) {
+      a.scal_w[SC_RR_RHO + a.iter] = rr_r;
+      a.scal_w[SC_RR_CHAT + a.iter] = rr_c;
+      a.scal_w[SC_RR_RHO + a.iter + 1] = nr;
+      a.scal_w[SC_RR_CHAT + a.iter + 1] = nc;
+    }
+  }
+  if (bid == 0 && tid == 0) {
+    a.scal_w[SC_PAP_RHO + a.iter] = red[0];
+    a.scal_w[SC_PAP_CHAT + a.iter] = red[1];
+  }
+
+  if (last) {
+    // Newton update x_{n+1} = x_n + dx + gamma_{L-1} p_{L-1} (Eq. 3) on this tile and stripe
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int k = S::out_idx(t, e);
+      const size_t i = j * N + (size_t)k * L + x;
+      const float2 pv = buf(k);
+      const float2 dv = hasdx ? pf[k * CW + c] : make_float2(0.f, 0.f);
+      float2 xv = a.xc[i];
+      xv.x += fmaf(gamma, pv.x, dv.x);
+      xv.y += fmaf(gamma, pv.y, dv.y);
+      a.xc[i] = xv;
+    }
+    for (size_t i = lo + tid; i < hi; i += blockDim.x) {
+      const float2 pv = a.rho_a[i];
+      const float2 dv = hasdx ? a.rho_dx[i] : make_float2(0.f, 0.f);
+      float2 xv = a.x_rho[i];
+      xv.x += fmaf(gamma, pv.x, dv.x);
+      xv.y += fmaf(gamma, pv.y, dv.y);
+      a.x_rho[i] = xv;
+    }
+    return;
+  }
+
+  // r_{i+1} = r - gamma Ap; dx += gamma p; p_{i+1} = r_{i+1} + beta p; t = w^-1 p_{i+1} (K1 prologue)
+  {
+    constexpr int CH = 8;
+#pragma unroll
+    for (int e0 = 0; e0 < E; e0 += CH) {
+      float wv[CH];
+      float2 dv[CH];
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const size_t ii = (size_t)S::out_idx(t, e0 + u) * L + x;
+        wv[u] = a.winv[ii];
+        dv[u] = hasdx ? a.dx[j * N + ii] : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const int k = S::out_idx(t, e0 + u);
+        const size_t i = j * N + (size_t)k * L + x;
+        const float2 rv = pf[k * CW + c], pv = buf(k);
+        const float2 rn = make_float2(fmaf(-gamma, v[e0 + u].x, rv.x), fmaf(-gamma, v[e0 + u].y, rv.y));
+        a.r[i] = rn;
+        a.dx[i] = make_float2(fmaf(gamma, pv.x, dv[u].x), fmaf(gamma, pv.y, dv[u].y));
+        const float2 pn = make_float2(fmaf(beta, pv.x, rn.x), fmaf(beta, pv.y, rn.y));
+        a.p[i] = pn;
+        v[e0 + u] = cscale(pn, wv[u] * sgn_of(k));
+      }
+    }
+  }
+  for (size_t i = lo + tid; i < hi; i += blockDim.x) {
+    const float2 av = a.rho_out[i], rv = a.rho_r[i], pv = a.rho_a[i];
+    const float2 dv = hasdx ? a.rho_dx[i] : make_float2(0.f, 0.f);
+    const float2 rn = make_float2(fmaf(-gamma, av.x, rv.x), fmaf(-gamma, av.y, rv.y));
+    a.rho_r[i] = rn;
+    a.rho_dx[i] = make_float2(fmaf(gamma, pv.x, dv.x), fmaf(gamma, pv.y, dv.y));
+    a.rho_p[i] = make_float2(fmaf(beta, pv.x, rn.x), fmaf(beta, pv.y, rn.y));
+  }
+  trace_stamp(a.trace, 4);
+  __syncthreads();   // every parked p has been read: xb becomes the exchange buffer again
+  out_to_in<L>(v, t, buf, SyncBlock{});
+  fft<L, +1>(v, t, tw, buf, SyncBlock{});
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    if (out_is_omega<L>(e)) {
+      const int k = S::out_idx(t, e);
+      a.t1[j * H + (size_t)(k - q) * L + x] = cscale(v[e], invL * sgn_of(k));
+    }
+  }
+}
+
+template <int L>
+__global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) k5cg_kernel(ColArgs a, const float2* __restrict__ twg) {
+  constexpr int CW = ColGeo<L>::CW;
+  extern __shared__ float4 smem_raw[];
+  float2* tw = reinterpret_cast<float2*>(smem_raw);
+  float2* xb = tw + L;
+  double* red = reinterpret_cast<double*>(xb + (size_t)L * CW);   // 128 doubles
+  float2* pf = reinterpret_cast<float2*>(red + 128);
+  trace_stamp(a.trace, 0);
+  tw_copy_async(tw, twg, L);
+  pdl_wait();
+  pdl_trigger();
+  k5cg_task<L>(a, tw, xb, pf, red);
+  trace_stamp(a.trace, 5);
   trace_stamp(a.trace, 6);
 }
 
@@ -860,7 +1151,7 @@ __device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, int jlo, i
     __syncthreads();
     for (int xx = tid; xx < n; xx += nt) {
       float2 sacc = accs[xx];
-      for (int gg = 0; gg < GPC && j0 + gg < jhi; ++gg) sacc = cadd(sacc, xbase[(size_t)gg * L + xx]);
+      for (int gg = 0; gg < GPC && j0 + gg < jhi; ++gg) sacc = cadd(sacc, xbase[(size_t)gg * L + rsw(xx)]);
       accs[xx] = sacc;
     }
     __syncthreads();
@@ -1514,6 +1805,29 @@ static bool col_fusable_l(int J) {
   return (long long)(L / ColGeo<L>::CW) * J <= (long long)per * nsm;
 }
 
+// ... and the single-barrier k5cg_kernel (larger shared memory: the prefetch tile)
+template <int L>
+static bool k5cg_fusable_l(int J) {
+  if (ColGeo<L>::THREADS < 64) return false;
+  auto kern = k5cg_kernel<L>;
+  const size_t smem = ColGeo<L>::SMEM_PF;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return false;
+  int dev = 0, nsm = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, ColGeo<L>::THREADS, smem) != cudaSuccess) return false;
+  return (long long)(L / ColGeo<L>::CW) * J <= (long long)per * nsm;
+}
+
+template <int L>
+static cudaError_t launch_k5cg_t(const ColArgs& a, const float2* tw, cudaStream_t s) {
+  auto kern = k5cg_kernel<L>;
+  const size_t smem = ColGeo<L>::SMEM_PF;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_coop(kern, dim3(L / ColGeo<L>::CW, a.J), dim3(ColGeo<L>::THREADS), smem, s, a, tw);
+}
+
 template <int L, int MODE>
 static cudaError_t launch_col_t(const ColArgs& a, const float2* tw, cudaStream_t s) {
   auto kern = col_kernel<L, MODE>;
@@ -1539,6 +1853,7 @@ static cudaError_t launch_col_l(int mode, const ColArgs& a, const float2* tw, cu
     case CK_FFT_W_NORMAL: return launch_col_t<L, CK_FFT_W_NORMAL>(a, tw, s);
     case CK_FFT_W_RHS: return launch_col_t<L, CK_FFT_W_RHS>(a, tw, s);
     case CK_FFT_W_ADJ: return launch_col_t<L, CK_FFT_W_ADJ>(a, tw, s);
+    case CK_K5CG: return launch_k5cg_t<L>(a, tw, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -1671,7 +1986,8 @@ static cudaError_t launch_fft2d_l(const float2* in, float2* out, int batch, int 
   int col_tiles_##L();                                                                          \
   cudaError_t launch_frame_##L(const FrameArgs& f, cudaStream_t s);                             \
   bool frame_ok_##L();                                                                          \
-  bool col_fusable_##L(int J);
+  bool col_fusable_##L(int J);                                                                  \
+  bool k5cg_fusable_##L(int J);
 #define NLV_INSTANTIATE(L)                                                                       \
   cudaError_t launch_col_##L(int mode, const ColArgs& a, const float2* tw, cudaStream_t s) {    \
     return launch_col_l<L>(mode, a, tw, s);                                                      \
@@ -1686,7 +2002,8 @@ static cudaError_t launch_fft2d_l(const float2* in, float2* out, int batch, int 
   int col_tiles_##L() { return L / ColGeo<L>::CW; }                                             \
   cudaError_t launch_frame_##L(const FrameArgs& f, cudaStream_t s) { return launch_frame_l<L>(f, s); } \
   bool frame_ok_##L() { return FrameGeo<L>::kOk; }                                              \
-  bool col_fusable_##L(int J) { return col_fusable_l<L>(J); }
+  bool col_fusable_##L(int J) { return col_fusable_l<L>(J); }                                   \
+  bool k5cg_fusable_##L(int J) { return k5cg_fusable_l<L>(J); }
 
 #define NLV_FOR_EACH_NG(X) X(16) X(32) X(48) X(64) X(96) X(128) X(192) X(256) X(384) X(512) X(768) X(1024)
 NLV_FOR_EACH_NG(NLV_DECLARE)

@@ -69,6 +69,7 @@ struct nlinv_plan_s {
   bool rho_spread = true;                 // rho block in stripes over the coil tiles (NLINV_RHO_SPREAD=0: own CTAs)
   bool fuse_k5 = false;                   // K5 + r update as one cooperative pass (world == 1, fits one wave)
   bool fuse_k1 = false;                   // ... also K1 of the next iteration / the Newton update
+  bool k5cg1 = false;                     // fused K5 + CG + K1 with a single grid barrier (k5cg_kernel)
   unsigned* kbar = nullptr;               // its grid barrier
   double* kpart = nullptr;                // its <p, Ap> partials
   unsigned long long* trace = nullptr;
@@ -325,9 +326,12 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
     pl->fuse_k5 = pl->rho_spread && pl->world == 1 && !(fk && fk[0] == '0') && col_fusable(nx, pl->J);
     if (pl->fuse_k5) {
       ok &= alloc((void**)&pl->kbar, sizeof(unsigned) * 2);
-      ok &= alloc((void**)&pl->kpart, sizeof(double) * 4 * kMaxRedBlocks);
+      ok &= alloc((void**)&pl->kpart, sizeof(double) * 8 * kMaxRedBlocks);
       const char* f1 = std::getenv("NLINV_FUSE_K1");
       pl->fuse_k1 = !(f1 && f1[0] == '0');
+      // one grid barrier per CG iteration (k5cg_kernel, R19) unless NLINV_K5CG1=0
+      const char* g1 = std::getenv("NLINV_K5CG1");
+      pl->k5cg1 = pl->fuse_k1 && !(g1 && g1[0] == '0') && k5cg_fusable(nx, pl->J);
     }
   }
   {
@@ -431,7 +435,7 @@ extern "C" long long nlinv_plan_launch_count(nlinv_plan pl) { return pl ? pl->la
 namespace {
 
 const char* kColNames[] = {"col_ifft_w", "col_ifft_w_cg", "col_fwdp", "col_psf", "col_resadj", "col_adj1",
-                           "col_fft_w_normal", "col_fft_w_rhs", "col_fft_w_adj"};
+                           "col_fft_w_normal", "col_fft_w_rhs", "col_fft_w_adj", "col_k5cg"};
 const char* kRowNames[] = {"row_setpoint", "row_setpoint_fwd", "row_rss", "row_k2", "row_k4"};
 
 struct Enq {
@@ -458,7 +462,9 @@ struct Enq {
     return NLINV_OK;
   }
   nlinv_status col(int mode, ColArgs a) {
-    a.trace = (pl->trace_mode == mode) ? pl->trace : nullptr;
+    // the fused K5 + CG pass is traced at CG iteration 1 only (a steady-state K5 -> CG -> K1 launch)
+    const bool fused = (mode == CK_FFT_W_NORMAL && a.fuse_update) || mode == CK_K5CG;
+    a.trace = (pl->trace_mode == mode && (!fused || (a.iter == 1 && a.fuse_k1))) ? pl->trace : nullptr;
     a.rho_spread = pl->rho_spread ? 1 : 0;
     a.winv = pl->winv;
     a.mask = pl->mask;
@@ -470,6 +476,7 @@ struct Enq {
     if (mode == CK_FFT_W_NORMAL && a.fuse_update)
       name = a.fuse_k1 ? "col_k5_cg_k1" : (a.fuse_newton ? "col_k5_newton" : "col_fft_w_normal_upd");
     if (mode == CK_FFT_W_RHS && a.fuse_k1) name = "col_rhs_k1";
+    if (mode == CK_K5CG) name = a.fuse_k1 ? "col_k5_cg_k1" : "col_k5_newton";
     return kern(name, [&] { return launch_col(pl->ng, mode, a, pl->tw, s); });
   }
   nlinv_status row(int mode, RowArgs a) {
@@ -753,7 +760,7 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
         c5.bar_count = pl->kbar;
         c5.bar_gen = pl->kbar + 1;
         c5.fpart = pl->kpart;
-        TRY(q.col(CK_FFT_W_NORMAL, c5));
+        TRY(q.col(pl->k5cg1 ? CK_K5CG : CK_FFT_W_NORMAL, c5));
       }
       continue;
     }

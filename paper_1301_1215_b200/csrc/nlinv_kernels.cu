@@ -275,6 +275,13 @@ bool col_fusable(int ng, int J) {
 #undef X
   return false;
 }
+
+bool k5cg_fusable(int ng, int J) {
+#define X(L) if (ng == L) return k5cg_fusable_##L(J);
+  NLV_FOR_EACH_NG(X)
+#undef X
+  return false;
+}
 bool frame_supported(int ng) {
 #define X(L) if (ng == L) return frame_ok_##L();
   NLV_FOR_EACH_NG(X)

@@ -31,6 +31,7 @@ enum ColMode {
   CK_FFT_W_NORMAL, // K5: column FFT -> Ap = w^-1 . + alpha p (+<p,Ap>)
   CK_FFT_W_RHS,    // Newton rhs: b = w^-1 . - alpha (chat - chat_ref); r = p = b (+<b,b>)
   CK_FFT_W_ADJ,    // adjoint tail: w^-1 . (no alpha)
+  CK_K5CG,         // K5 + CG step + K1 (or Newton update), one grid barrier (k5cg_kernel)
 };
 
 // Row-kernel modes (one CTA = one Omega row of all local coils).
@@ -75,7 +76,7 @@ struct ColArgs {
   int last_iter;           // K5 fused: last CG iteration (no r update needed)
   unsigned* bar_count;     // grid barrier of the fused K5
   unsigned* bar_gen;
-  double* fpart;           // [4 * blocks] <p, Ap> and <r, r> partials of the fused K5
+  double* fpart;           // [6 * blocks] dot partials of the fused K5 passes
   int fuse_k1;             // fused K5 / rhs: also run K1 of the next CG iteration (T1 into t1)
   int fuse_newton;         // fused K5, last iteration: also x += dx + gamma p
   float2* t1;              // K1 output (half image) for the fused variants
@@ -164,6 +165,7 @@ int mask_count_blocks(int N);
 cudaError_t launch_scatter_samples(const float2* samples, const int* idx, const int* nnz, int nnz_cap, int J,
                                    size_t N, float2* y, cudaStream_t s);
 bool col_fusable(int ng, int J);
+bool k5cg_fusable(int ng, int J);
 cudaError_t launch_coil_sum(int ng, const float2* S_all, int J, float2* S, cudaStream_t s);
 cudaError_t launch_rss_sum(int ng, const float* rss_all, int J, float* rss, cudaStream_t s);
 

@@ -303,7 +303,8 @@ def test_reconstruct_c2_full_frame():
 
 
 VARIANTS = {
-    "fused (default)": {},
+    "fused (default, one grid barrier per CG iteration)": {},
+    "fused, two grid barriers": {"NLINV_K5CG1": "0"},
     "unfused K1/K5": {"NLINV_FUSE_K1": "0", "NLINV_FUSE_K5": "0"},
     "K5+update only": {"NLINV_FUSE_K1": "0"},
     "rho in own CTAs": {"NLINV_RHO_SPREAD": "0"},
