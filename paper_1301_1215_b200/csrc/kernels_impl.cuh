@@ -144,6 +144,28 @@ __device__ __forceinline__ void grid_barrier_n(unsigned* count, unsigned* gen, u
   __syncthreads();
 }
 
+// Grid barrier with one atomic per CTA and no reset: CTA 0 adds 2^31 - (nb - 1), every other CTA
+// adds 1, so the word's top bit flips exactly when the last CTA arrives and the low bits return to
+// their value (reusable across launches and graph replays). Waiters poll with ld.acquire.gpu.
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void grid_sync_flip(unsigned* bar, unsigned nb, bool master) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned inc = master ? (0x80000000u - (nb - 1u)) : 1u;
+    __threadfence();   // release: this CTA's writes (ordered before by bar.sync) precede the arrival
+    const unsigned old = atomicAdd(bar, inc);
+    unsigned spins = 0;
+    while (((old ^ ld_acquire_gpu(bar)) & 0x80000000u) == 0u) {
+      if (++spins > (1u << 30)) __trap();  // never hang the GPU: abort the context instead
+    }
+  }
+  __syncthreads();
+}
+
 // Textbook CG scalars (R9): gamma_i = rr_i / <p_i, A p_i>, beta_i = rr_{i+1} / rr_i.
 // rr_i and <p_i, A p_i> are published as (rho, chat) parts; rho is replicated and counted once.
 __device__ __forceinline__ double cg_rr(const double* scal, int i) { return scal[SC_RR_RHO + i] + scal[SC_RR_CHAT + i]; }
@@ -755,28 +777,61 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
     }
   }
 
-  // rho block stripe of this tile: A p_rho = M sum_s S_s + alpha p_rho (replicated rho)
+  // rho block stripe of this tile: A p_rho = M sum_s S_s + alpha p_rho (replicated rho).
+  // Dot partials in fp64 per term: fp32 products underflow once CG has driven r, p to ~1e-20
+  // (the first Newton step from rho = 1, chat = 0 reaches ||r|| ~ 1e-30), giving 0/0.
   double d[NV] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   constexpr int NTILE = L / CW;
   const int nstripe = a.J * NTILE, stripe = j * NTILE + tile;
   const size_t chunk = (N + nstripe - 1) / nstripe;
   const size_t lo = (size_t)stripe * chunk, hi = (lo + chunk < N) ? lo + chunk : N;
-  for (size_t i = lo + tid; i < hi; i += blockDim.x) {
+  // stripe values stay in registers when the stripe is <= SR elements per thread (C2: 2); the
+  // loads of all SR elements are issued together
+  constexpr int SR = 2;
+  const bool sreg = (hi - lo) <= (size_t)SR * blockDim.x;
+  float2 so[SR], sp[SR], sr[SR];
+  auto stripe_sum = [&](size_t i) {
     const int y = (int)(i / L), xx = (int)(i % L);
     float2 sv = make_float2(0.f, 0.f);
     if (xx >= q && xx < q + n && y >= q && y < q + n) {
       const size_t o = (size_t)(y - q) * n + (xx - q);
-      for (int sp = 0; sp < a.nS; ++sp) sv = cadd(sv, a.S[sp * Qs + o]);
+      for (int s2 = 0; s2 < a.nS; ++s2) sv = cadd(sv, a.S[s2 * Qs + o]);
     }
-    const float2 pv = a.rho_a[i];
-    const float2 o = make_float2(fmaf(a.alpha, pv.x, sv.x), fmaf(a.alpha, pv.y, sv.y));
-    a.rho_out[i] = o;
-    d[0] += (double)pv.x * o.x + (double)pv.y * o.y;
-    if (!last) {
-      const float2 rv = a.rho_r[i];
+    return sv;
+  };
+  if (sreg) {
+    float2 sv[SR];
+#pragma unroll
+    for (int u = 0; u < SR; ++u) {
+      const size_t i = lo + tid + (size_t)u * blockDim.x;
+      const bool ok = i < hi;
+      sp[u] = ok ? a.rho_a[i] : make_float2(0.f, 0.f);
+      sr[u] = (ok && !last) ? a.rho_r[i] : make_float2(0.f, 0.f);
+      sv[u] = ok ? stripe_sum(i) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < SR; ++u) {
+      const float2 pv = sp[u], rv = sr[u];
+      const float2 o = make_float2(fmaf(a.alpha, pv.x, sv[u].x), fmaf(a.alpha, pv.y, sv[u].y));
+      so[u] = o;
+      d[0] += (double)pv.x * o.x + (double)pv.y * o.y;
       d[2] += (double)rv.x * o.x + (double)rv.y * o.y;
       d[4] += (double)o.x * o.x + (double)o.y * o.y;
       d[6] += (double)rv.x * rv.x + (double)rv.y * rv.y;
+    }
+  } else {
+    for (size_t i = lo + tid; i < hi; i += blockDim.x) {
+      const float2 sv = stripe_sum(i);
+      const float2 pv = a.rho_a[i];
+      const float2 o = make_float2(fmaf(a.alpha, pv.x, sv.x), fmaf(a.alpha, pv.y, sv.y));
+      a.rho_out[i] = o;
+      d[0] += (double)pv.x * o.x + (double)pv.y * o.y;
+      if (!last) {
+        const float2 rv = a.rho_r[i];
+        d[2] += (double)rv.x * o.x + (double)rv.y * o.y;
+        d[4] += (double)o.x * o.x + (double)o.y * o.y;
+        d[6] += (double)rv.x * rv.x + (double)rv.y * rv.y;
+      }
     }
   }
 
@@ -835,7 +890,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
       for (int ww = 0; ww < nw; ++ww) sk += red[8 + ww * NV + tid];
       a.fpart[tid * nb + bid] = sk;
     }
-    grid_barrier_n(a.bar_count, a.bar_gen, nb);
+    grid_sync_flip(a.bar_count + 2, nb, bid == 0);
     trace_stamp(a.trace, 3);
     // totals: warp w sums value k = w (+ nw ...) over all CTAs in a fixed order -> identical in every CTA
     for (int k = w; k < NV; k += nw) {
@@ -884,13 +939,21 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
       xv.y += fmaf(gamma, pv.y, dv.y);
       a.xc[i] = xv;
     }
-    for (size_t i = lo + tid; i < hi; i += blockDim.x) {
-      const float2 pv = a.rho_a[i];
+    auto newton_rho = [&](size_t i, float2 pv) {
       const float2 dv = hasdx ? a.rho_dx[i] : make_float2(0.f, 0.f);
       float2 xv = a.x_rho[i];
       xv.x += fmaf(gamma, pv.x, dv.x);
       xv.y += fmaf(gamma, pv.y, dv.y);
       a.x_rho[i] = xv;
+    };
+    if (sreg) {
+#pragma unroll
+      for (int u = 0; u < SR; ++u) {
+        const size_t i = lo + tid + (size_t)u * blockDim.x;
+        if (i < hi) newton_rho(i, sp[u]);
+      }
+    } else {
+      for (size_t i = lo + tid; i < hi; i += blockDim.x) newton_rho(i, a.rho_a[i]);
     }
     return;
   }
@@ -922,13 +985,21 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
       }
     }
   }
-  for (size_t i = lo + tid; i < hi; i += blockDim.x) {
-    const float2 av = a.rho_out[i], rv = a.rho_r[i], pv = a.rho_a[i];
+  auto update_rho = [&](size_t i, float2 av, float2 rv, float2 pv) {
     const float2 dv = hasdx ? a.rho_dx[i] : make_float2(0.f, 0.f);
     const float2 rn = make_float2(fmaf(-gamma, av.x, rv.x), fmaf(-gamma, av.y, rv.y));
     a.rho_r[i] = rn;
     a.rho_dx[i] = make_float2(fmaf(gamma, pv.x, dv.x), fmaf(gamma, pv.y, dv.y));
     a.rho_p[i] = make_float2(fmaf(beta, pv.x, rn.x), fmaf(beta, pv.y, rn.y));
+  };
+  if (sreg) {
+#pragma unroll
+    for (int u = 0; u < SR; ++u) {
+      const size_t i = lo + tid + (size_t)u * blockDim.x;
+      if (i < hi) update_rho(i, so[u], sr[u], sp[u]);
+    }
+  } else {
+    for (size_t i = lo + tid; i < hi; i += blockDim.x) update_rho(i, a.rho_out[i], a.rho_r[i], a.rho_a[i]);
   }
   trace_stamp(a.trace, 4);
   __syncthreads();   // every parked p has been read: xb becomes the exchange buffer again

@@ -325,7 +325,7 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
     const char* fk = std::getenv("NLINV_FUSE_K5");
     pl->fuse_k5 = pl->rho_spread && pl->world == 1 && !(fk && fk[0] == '0') && col_fusable(nx, pl->J);
     if (pl->fuse_k5) {
-      ok &= alloc((void**)&pl->kbar, sizeof(unsigned) * 2);
+      ok &= alloc((void**)&pl->kbar, sizeof(unsigned) * 4);   // [count, gen] + k5cg flip word
       ok &= alloc((void**)&pl->kpart, sizeof(double) * 8 * kMaxRedBlocks);
       const char* f1 = std::getenv("NLINV_FUSE_K1");
       pl->fuse_k1 = !(f1 && f1[0] == '0');
@@ -376,7 +376,7 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
   if (e == cudaSuccess) e = cudaMemset(pl->scal, 0, sizeof(double) * SC_TOTAL);
   if (e == cudaSuccess) e = cudaMemset(pl->counter, 0, sizeof(unsigned) * 4);
   if (e == cudaSuccess && pl->fbar) e = cudaMemset(pl->fbar, 0, sizeof(unsigned) * 2);
-  if (e == cudaSuccess && pl->kbar) e = cudaMemset(pl->kbar, 0, sizeof(unsigned) * 2);
+  if (e == cudaSuccess && pl->kbar) e = cudaMemset(pl->kbar, 0, sizeof(unsigned) * 4);
   if (e != cudaSuccess) {
     std::string msg = std::string("plan upload: ") + cudaGetErrorString(e);
     plan_free(pl);

@@ -20,17 +20,21 @@ rows = tr[(tr[:, 0] > 0)]
 t0 = rows[:, 0].min()
 rel = (rows - t0) / 1e3
 names = ["start", "tw+loads issued", "fft1 done", "mid done", "fft2 done", "epilogue done", "reduce done"]
+if mode == 9:  # k5cg_kernel (one barrier): 7 = epilogue + dots done, 3 = barrier passed, 4 = updates done
+    order = [0, 1, 2, 7, 3, 4, 5, 6]
+    names6 = ["start", "prologue + rho stripe", "K5 fft done", "Ap + dots done", "barrier passed",
+              "r/dx/p update done", "K1 fft + T1 store", "end"]
 if mode == 6:  # fused K5 + CG + K1 (iteration 1): 7 = epilogue done, 3 = barrier 1 passed, 4 = barrier 2 passed
     order = [0, 1, 2, 7, 3, 4, 5, 6]
     names6 = ["start", "prologue loads issued", "K5 fft done", "Ap + <p,Ap> done", "barrier 1 passed",
               "r update + barrier 2", "p update + K1 fft + store", "end"]
     tr0 = plan.trace_read().astype(np.float64) if False else None
 print(f"mode {mode}: {len(rows)} CTAs; kernel span {(rows[:, 6].max() - t0)/1e3:.2f} us")
-if mode == 6:
+if mode in (6, 9):
     rows = rows[:, order]
     rel = (rows - t0) / 1e3
     names = names6
-for k in range(1, 8 if mode == 6 else 7):
+for k in range(1, 8 if mode in (6, 9) else 7):
     ok = rows[:, k] > 0
     if ok.sum() == 0: continue
     d = (rows[ok, k] - rows[ok, k - 1 if rows[ok, k-1].min() > 0 else 0]) / 1e3
