@@ -220,6 +220,46 @@ nlinv_status nlinv_debug_fft2d(nlinv_plan plan, const nlinv_c32* in, nlinv_c32* 
 /* Number of kernels this library enqueued since plan creation (launch-count evidence). */
 long long nlinv_plan_launch_count(nlinv_plan plan);
 
+/* ---------------------------------------------------------------------------------------------
+ * PCA channel compression. PAPER P:241 (§3.2): "A principal component
+ * analysis preprocessing step is applied before reconstruction to compress the 32 channels to
+ * 8-12"; covariance C = sum_n y[n] y[n]^H (J x J), eigendecomposition, projection
+ * y'_k = v_k^H y onto the top-J' eigenvectors (descending eigenvalues), each v_k scaled by a unit
+ * phase so that its largest-magnitude component (first index on ties) is real-positive.
+ * Channel data Y: device c32 [J][nsamp] (channel rows, any sample set: a full gridded frame or
+ * its compact samples). A handle owns its workspace; not thread-safe; plan-independent.
+ * ------------------------------------------------------------------------------------------- */
+typedef struct nlinv_pca_s* nlinv_pca;
+
+/* 1 <= J <= 32 channels (ERR_SIZE otherwise), 1 <= Jc <= J kept components (ERR_ARG). Allocates
+ * on the current CUDA device (ERR_NOMEM). */
+nlinv_status nlinv_pca_create(int J, int Jc, nlinv_pca* out);
+nlinv_status nlinv_pca_destroy(nlinv_pca pca);
+
+/* Fit: C (fp64, deterministic CTA-order reduction), Jacobi eigendecomposition (fp64), V. Enqueued
+ * on `stream`, no host sync. Y: device [J][nsamp], nsamp >= 1. */
+nlinv_status nlinv_pca_fit(nlinv_pca pca, const nlinv_c32* Y, long long nsamp, void* stream);
+
+/* Host readback of the last fit (synchronises the device). Any output may be NULL.
+ * V_host: c32 [J][Jc] row-major (V[j*Jc + k] = component j of v_k); eig_host: fp64 [J] descending;
+ * energy: captured fraction sum_{k<Jc} lambda_k / sum_k lambda_k (negative rounding clipped to 0);
+ * cov_host: fp64 [J][J][2] (re, im) covariance. ERR_STATE before any fit / set_matrix. */
+nlinv_status nlinv_pca_result(nlinv_pca pca, nlinv_c32* V_host, double* eig_host, double* energy,
+                              double* cov_host);
+
+/* Use a given compression matrix (host c32 [J][Jc]) instead of a fit, e.g. one fitted on the
+ * first frame of a stream. */
+nlinv_status nlinv_pca_set_matrix(nlinv_pca pca, const nlinv_c32* V_host);
+
+/* Apply: out[k][n] = sum_j conj(V[j][k]) Y[j][n] (channels summed in ascending order, fp32).
+ * Y: device [J][nsamp]; out: device [Jc][nsamp], must not overlap Y (ERR_ARG). ERR_STATE before
+ * any fit / set_matrix. Enqueued on `stream`. */
+nlinv_status nlinv_pca_apply(nlinv_pca pca, const nlinv_c32* Y, long long nsamp, nlinv_c32* out, void* stream);
+
+/* Last error message of this handle (never NULL) and its number of enqueued kernels. */
+const char* nlinv_pca_last_error(nlinv_pca pca);
+long long nlinv_pca_launch_count(nlinv_pca pca);
+
 #ifdef __cplusplus
 }
 #endif

@@ -54,7 +54,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for L in SIZES:
         jobs.append(([nvcc, *ARCH, *FLAGS, *defs, f"-DNLV_L={L}", "-c", os.path.join(CSRC, "inst.cu"),
                       "-o", os.path.join(OBJ, f"inst_{L}.o")], f"inst_{L}"))
-    for name in ("nlinv_kernels", "nlinv_capi"):
+    for name in ("nlinv_kernels", "nlinv_capi", "pca"):
         jobs.append(([nvcc, *ARCH, *FLAGS, *defs, "-c", os.path.join(CSRC, name + ".cu"),
                       "-o", os.path.join(OBJ, name + ".o")], name))
 
@@ -69,8 +69,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=max(2, os.cpu_count() or 2)) as ex:
         list(ex.map(run, jobs))
-    objs = [os.path.join(OBJ, f"inst_{L}.o") for L in SIZES] + [os.path.join(OBJ, "nlinv_kernels.o"),
-                                                                 os.path.join(OBJ, "nlinv_capi.o")]
+    objs = [os.path.join(OBJ, f"inst_{L}.o") for L in SIZES] + [os.path.join(OBJ, n + ".o")
+                                                                 for n in ("nlinv_kernels", "nlinv_capi", "pca")]
     link = [nvcc, *ARCH, "-shared", "-o", LIB + ".tmp", *objs]
     if nccl_lib:
         link += ["-L" + nccl_lib, "-l:libnccl.so.2", "-Xlinker", "-rpath," + nccl_lib]

@@ -112,6 +112,10 @@ struct nlinv_plan_s {
 #endif
 };
 
+namespace nlv {
+void set_lib_error(const std::string& msg) { g_lib_error = msg; }   // pca.cu
+}  // namespace nlv
+
 static nlinv_status fail(nlinv_plan pl, nlinv_status s, const std::string& msg) {
   if (pl) pl->err = msg;
   g_lib_error = msg;

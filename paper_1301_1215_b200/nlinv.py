@@ -74,6 +74,14 @@ _SIGS = {
     "nlinv_plan_phase_times": (c_int, [c_void_p, c_int, c_void_p, c_int, ctypes.POINTER(c_int)]),
     "nlinv_plan_trace": (c_int, [c_void_p, c_int, c_void_p, c_int]),
     "nlinv_plan_profile_json": (c_int, [c_void_p, ctypes.c_char_p, ctypes.c_size_t]),
+    "nlinv_pca_create": (c_int, [c_int, c_int, ctypes.POINTER(c_void_p)]),
+    "nlinv_pca_destroy": (c_int, [c_void_p]),
+    "nlinv_pca_fit": (c_int, [c_void_p, c_void_p, c_ll, c_void_p]),
+    "nlinv_pca_result": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "nlinv_pca_set_matrix": (c_int, [c_void_p, c_void_p]),
+    "nlinv_pca_apply": (c_int, [c_void_p, c_void_p, c_ll, c_void_p, c_void_p]),
+    "nlinv_pca_last_error": (ctypes.c_char_p, [c_void_p]),
+    "nlinv_pca_launch_count": (c_ll, [c_void_p]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -343,6 +351,74 @@ class Plan:
     def close(self):
         if getattr(self, "_h", None):
             _lib.nlinv_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Pca:
+    """PCA channel compression through the C ABI (nlinv_pca_*).
+    Argument marshalling only: the covariance, eigensolver and projection run in libnlinv.so."""
+
+    def __init__(self, ncoils: int, keep: int):
+        self.J, self.Jc = int(ncoils), int(keep)
+        h = c_void_p()
+        _check(_lib.nlinv_pca_create(self.J, self.Jc, ctypes.byref(h)))
+        self._h = h
+
+    def _chk(self, st):
+        if st != 0:
+            raise NlinvError(st, _lib.nlinv_status_string(st).decode(), _lib.nlinv_pca_last_error(self._h).decode())
+
+    def _data(self, Y):
+        import torch
+        if not (isinstance(Y, torch.Tensor) and Y.is_cuda and Y.dtype == torch.complex64 and Y.is_contiguous()
+                and Y.shape[0] == self.J):
+            raise ValueError(f"Y must be a contiguous CUDA complex64 tensor with {self.J} channel rows")
+        return Y.numel() // self.J
+
+    def fit(self, Y, stream=None):
+        n = self._data(Y)
+        self._chk(_lib.nlinv_pca_fit(self._h, ctypes.c_void_p(Y.data_ptr()), n, _stream_ptr(stream)))
+        return self
+
+    def result(self):
+        """(V [J, Jc] complex64, eigenvalues [J] float64 descending, energy fraction, C [J, J] complex128)"""
+        V = np.zeros((self.J, self.Jc), dtype=np.complex64)
+        w = np.zeros(self.J, dtype=np.float64)
+        e = ctypes.c_double()
+        C = np.zeros((self.J, self.J), dtype=np.complex128)
+        self._chk(_lib.nlinv_pca_result(self._h, V.ctypes.data, w.ctypes.data, ctypes.byref(e), C.ctypes.data))
+        return V, w, e.value, C
+
+    def set_matrix(self, V):
+        V = np.ascontiguousarray(V, dtype=np.complex64)
+        if V.shape != (self.J, self.Jc):
+            raise ValueError(f"V must be [{self.J}, {self.Jc}]")
+        self._chk(_lib.nlinv_pca_set_matrix(self._h, V.ctypes.data))
+
+    def apply(self, Y, out=None, stream=None):
+        import torch
+        n = self._data(Y)
+        if out is None:
+            out = torch.empty((self.Jc,) + tuple(Y.shape[1:]), dtype=torch.complex64, device=Y.device)
+        if not (out.is_cuda and out.dtype == torch.complex64 and out.is_contiguous() and out.numel() == self.Jc * n):
+            raise ValueError("out must be a contiguous CUDA complex64 tensor with Jc channel rows")
+        self._chk(_lib.nlinv_pca_apply(self._h, ctypes.c_void_p(Y.data_ptr()), n, ctypes.c_void_p(out.data_ptr()),
+                                       _stream_ptr(stream)))
+        return out
+
+    @property
+    def launch_count(self) -> int:
+        return int(_lib.nlinv_pca_launch_count(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.nlinv_pca_destroy(self._h)
             self._h = None
 
     def __del__(self):
