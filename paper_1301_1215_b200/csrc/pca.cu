@@ -12,9 +12,9 @@
 //   C = V diag(lambda) V^H               jacobi_kernel: one CTA, parallel cyclic complex Jacobi in
 //                                          fp64 (round-robin pairing, J/2 disjoint rotations per
 //                                          step), then descending sort and the sign convention
-//   y'_k[n] = sum_j conj(V[j][k]) y_j[n] pca_apply_kernel: one sample per thread, coalesced
-//                                          channel rows, V in shared memory (HBM-bound: J reads and
-//                                          J' writes of 8 B per sample)
+//   y'_k[n] = sum_j conj(V[j][k]) y_j[n] pca_apply_kernel: two samples per thread, coalesced
+//                                          channel rows, V in shared memory (J reads and J' writes
+//                                          of 8 B per sample against J J' complex FMAs)
 // The covariance is a J x J x nsamp contraction (0.6 GFLOP for 32 coils on the 384^2 grid) fed by
 // one HBM pass over the data and run once per stream (the matrix is then applied to every frame),
 // so it uses register-blocked fp32 FMAs with fp64 accumulation across tiles rather than tensor
@@ -304,33 +304,67 @@ __global__ void __launch_bounds__(256) jacobi_kernel(const double* __restrict__ 
 }
 
 // ---------------------------------------------------------------- projection
-// out[k][n] = sum_j conj(V[j][k]) Y[j][n]; one sample per thread, channels in ascending order.
-constexpr int kApplyChunk = 16;
+// out[k][n] = sum_j conj(V[j][k]) Y[j][n], channels in ascending order. Each thread owns two
+// adjacent samples (one 16-byte load per channel row: coalesced) and a chunk of up to 16 outputs;
+// V sits in shared memory, read as float4 = two components (broadcast within a warp), so every
+// shared load feeds 4 complex FMAs.
+template <int KC>   // outputs per pass (V zero-padded to a multiple of KC: branch-free inner loop)
 __global__ void __launch_bounds__(256) pca_apply_kernel(const float2* __restrict__ V, const float2* __restrict__ Y, int J,
                                                         int Jc, long long nsamp, float2* __restrict__ out) {
-  __shared__ float2 Vs[kPcaMaxJ * kPcaMaxJ];
-  for (int i = threadIdx.x; i < J * Jc; i += blockDim.x) Vs[i] = V[i];
+  __shared__ __align__(16) float2 Vs[kPcaMaxJ * (kPcaMaxJ + 16)];
+  const int Jp = ((Jc + KC - 1) / KC) * KC;
+  for (int i = threadIdx.x; i < J * Jp; i += blockDim.x) {
+    const int j = i / Jp, k = i % Jp;
+    Vs[i] = (k < Jc) ? V[j * Jc + k] : make_float2(0.f, 0.f);
+  }
   __syncthreads();
-  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < nsamp; n += (long long)gridDim.x * blockDim.x) {
-    for (int k0 = 0; k0 < Jc; k0 += kApplyChunk) {
-      float2 acc[kApplyChunk];
+  const long long npair = (nsamp + 1) / 2;
+  const bool vec = (nsamp % 2) == 0;   // 16-byte aligned rows
+  for (long long pidx = blockIdx.x * (long long)blockDim.x + threadIdx.x; pidx < npair;
+       pidx += (long long)gridDim.x * blockDim.x) {
+    const long long n = 2 * pidx;
+    const bool two = (n + 1) < nsamp;
+    for (int k0 = 0; k0 < Jc; k0 += KC) {
+      float2 a0[KC], a1[KC];
 #pragma unroll
-      for (int kk = 0; kk < kApplyChunk; ++kk) acc[kk] = make_float2(0.f, 0.f);
-      for (int j = 0; j < J; ++j) {
-        const float2 y = Y[(size_t)j * nsamp + n];
-        const float2* vr = Vs + j * Jc + k0;
+      for (int kk = 0; kk < KC; ++kk) a0[kk] = a1[kk] = make_float2(0.f, 0.f);
+#pragma unroll 4
+      for (int j = 0; j < J; ++j) {   // unrolled so four channel loads are in flight together
+        float2 y0, y1;
+        if (vec) {
+          const float4 yy = __ldg(reinterpret_cast<const float4*>(Y + (size_t)j * nsamp + n));
+          y0 = make_float2(yy.x, yy.y);
+          y1 = make_float2(yy.z, yy.w);
+        } else {
+          y0 = Y[(size_t)j * nsamp + n];
+          y1 = two ? Y[(size_t)j * nsamp + n + 1] : make_float2(0.f, 0.f);
+        }
+        const float4* vr = reinterpret_cast<const float4*>(Vs + j * Jp + k0);
 #pragma unroll
-        for (int kk = 0; kk < kApplyChunk; ++kk) {
-          if (k0 + kk < Jc) {
-            const float2 v = vr[kk];   // conj(v) y
-            acc[kk].x = fmaf(v.x, y.x, fmaf(v.y, y.y, acc[kk].x));
-            acc[kk].y = fmaf(v.x, y.y, fmaf(-v.y, y.x, acc[kk].y));
-          }
+        for (int kp = 0; kp < KC / 2; ++kp) {
+          const float4 v = vr[kp];   // components k0+2kp (x, y) and k0+2kp+1 (z, w); conj(v) y
+          a0[2 * kp].x = fmaf(v.x, y0.x, fmaf(v.y, y0.y, a0[2 * kp].x));
+          a0[2 * kp].y = fmaf(v.x, y0.y, fmaf(-v.y, y0.x, a0[2 * kp].y));
+          a1[2 * kp].x = fmaf(v.x, y1.x, fmaf(v.y, y1.y, a1[2 * kp].x));
+          a1[2 * kp].y = fmaf(v.x, y1.y, fmaf(-v.y, y1.x, a1[2 * kp].y));
+          a0[2 * kp + 1].x = fmaf(v.z, y0.x, fmaf(v.w, y0.y, a0[2 * kp + 1].x));
+          a0[2 * kp + 1].y = fmaf(v.z, y0.y, fmaf(-v.w, y0.x, a0[2 * kp + 1].y));
+          a1[2 * kp + 1].x = fmaf(v.z, y1.x, fmaf(v.w, y1.y, a1[2 * kp + 1].x));
+          a1[2 * kp + 1].y = fmaf(v.z, y1.y, fmaf(-v.w, y1.x, a1[2 * kp + 1].y));
         }
       }
 #pragma unroll
-      for (int kk = 0; kk < kApplyChunk; ++kk)
-        if (k0 + kk < Jc) out[(size_t)(k0 + kk) * nsamp + n] = acc[kk];
+      for (int kk = 0; kk < KC; ++kk) {
+        if (k0 + kk < Jc) {
+          float2* o = out + (size_t)(k0 + kk) * nsamp + n;
+          if (vec) {
+            *reinterpret_cast<float4*>(o) = make_float4(a0[kk].x, a0[kk].y, a1[kk].x, a1[kk].y);
+          } else {
+            o[0] = a0[kk];
+            if (two) o[1] = a1[kk];
+          }
+        }
+      }
     }
   }
 }
@@ -454,11 +488,15 @@ extern "C" nlinv_status nlinv_pca_apply(nlinv_pca h, const nlinv_c32* Y, long lo
   if (nsamp < 1) return pfail(h, NLINV_ERR_ARG, "nsamp must be >= 1");
   if ((const void*)Y == (const void*)out) return pfail(h, NLINV_ERR_ARG, "in-place apply is not supported");
   cudaStream_t s = (cudaStream_t)stream;
-  long long nb = (nsamp + 255) / 256;
+  long long nb = ((nsamp + 1) / 2 + 255) / 256;
   const long long cap = 8LL * nlv::sm_count();
   if (nb > cap) nb = cap;
-  nlv::pca_apply_kernel<<<(int)nb, 256, 0, s>>>(h->V, reinterpret_cast<const float2*>(Y), h->J, h->Jc, nsamp,
-                                                reinterpret_cast<float2*>(out));
+  const float2* y = reinterpret_cast<const float2*>(Y);
+  float2* o = reinterpret_cast<float2*>(out);
+  if (h->Jc <= 4) nlv::pca_apply_kernel<4><<<(int)nb, 256, 0, s>>>(h->V, y, h->J, h->Jc, nsamp, o);
+  else if (h->Jc <= 8) nlv::pca_apply_kernel<8><<<(int)nb, 256, 0, s>>>(h->V, y, h->J, h->Jc, nsamp, o);
+  else if (h->Jc <= 12) nlv::pca_apply_kernel<12><<<(int)nb, 256, 0, s>>>(h->V, y, h->J, h->Jc, nsamp, o);
+  else nlv::pca_apply_kernel<16><<<(int)nb, 256, 0, s>>>(h->V, y, h->J, h->Jc, nsamp, o);
   PCU(cudaGetLastError());
   h->launches += 1;
   return NLINV_OK;

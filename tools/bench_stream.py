@@ -40,6 +40,8 @@ def main():
     ap.add_argument("--coils", type=int, default=32)
     ap.add_argument("--frames", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--compress", type=int, default=0,
+                    help="PCA-compress the coils to this many channels on the GPU before each frame (P:241)")
     args = ap.parse_args()
     J = args.coils
     t0 = time.perf_counter()
@@ -50,8 +52,14 @@ def main():
         masks.append(radial_mask(NG, SPOKES, TURNS, f))
     gen_s = time.perf_counter() - t0
 
-    plan = Plan(NG, J, masks[0])
+    Jr = args.compress if args.compress else J
+    plan = Plan(NG, Jr, masks[0])
     dframes = [torch.from_numpy(f).cuda() for f in frames]
+    pca = None
+    if args.compress:
+        from paper_1301_1215_b200 import Pca
+        pca = Pca(J, Jr).fit(dframes[0])          # compression matrix from the first frame
+        ycomp = torch.empty((Jr, NG, NG), dtype=torch.complex64, device="cuda")
     dmasks = [torch.from_numpy(m).cuda() for m in masks]
     x = torch.empty(plan.x_shape, dtype=torch.complex64, device="cuda")
     img = torch.empty(plan.image_shape, dtype=torch.complex64, device="cuda")
@@ -59,7 +67,10 @@ def main():
 
     def frame(i, first):
         plan.set_mask(dmasks[i % PERIOD])
-        plan.reconstruct(dframes[i % PERIOD], None if first else x, NEWTON, CG, x_out=x, image_out=img)
+        src = dframes[i % PERIOD]
+        if pca is not None:
+            src = pca.apply(src, ycomp)
+        plan.reconstruct(src, None if first else x, NEWTON, CG, x_out=x, image_out=img)
 
     frame(0, True)
     for i in range(1, args.warmup + 1):
@@ -77,6 +88,13 @@ def main():
     lat = [a.elapsed_time(b) for a, b in ev]
     total = g0.elapsed_time(g1)
 
+    if pca is not None:   # the streaming API takes already-compressed samples
+        out = {"config": f"C4 (1 GPU) with GPU PCA compression {J} -> {Jr} channels per frame", "coils": J,
+               "compressed_to": Jr, "energy_kept": pca.result()[2], "frames": args.frames,
+               "device": {"fps": round(args.frames / (total / 1e3), 2), "latency_ms_p50": round(pct(lat, 0.5), 4),
+                          "latency_ms_p95": round(pct(lat, 0.95), 4), "latency_ms_max": round(max(lat), 4)}}
+        print(json.dumps(out))
+        return
     # end to end through the public streaming API, one frame at a time
     hs = [torch.from_numpy(np.ascontiguousarray(f.reshape(J, -1)[:, np.flatnonzero(m)])).pin_memory()
           for f, m in zip(frames, masks)]
