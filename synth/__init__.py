@@ -143,3 +143,48 @@ def frame_inputs(ncoils: int, ng: int, t: float | None = None, norm: float | Non
     coils = coil_maps(ncoils, ng)
     y = acquire(embed(img, ng), coils, norm)
     return img, coils, y
+
+
+def radial_trajectory(ng: int, spokes: int, turns: int, frame: int) -> np.ndarray:
+    """k-space coordinates (kx, ky) in grid units from the grid centre of the radial spokes of one
+    frame (float64, [spokes, ng, 2]): spoke s at theta = pi (s T + (f mod T)) / (S T), samples at
+    r = i - ng/2 (SURVEY.md A12 / DESIGN.md R12). Acquisition geometry only: the assignment of
+    samples to grid cells (the gridding) is not done here."""
+    out = np.empty((spokes, ng, 2), dtype=np.float64)
+    for s in range(spokes):
+        theta = np.pi * (s * turns + (frame % turns)) / (spokes * turns)
+        r = np.arange(ng, dtype=np.float64) - ng // 2
+        out[s, :, 0] = r * np.cos(theta)
+        out[s, :, 1] = r * np.sin(theta)
+    return out
+
+
+def acquire_radial(image_grid: np.ndarray, coils: np.ndarray, traj: np.ndarray, scale: float = 1.0) -> np.ndarray:
+    """Non-Cartesian samples of Eq. 1 at the trajectory points: the sum over grid
+    points x of rho(x) c_j(x) e^{-2 pi i k.x / ng}, k and x from the grid centre, / ng, times
+    ``scale`` (complex128, [J, spokes, ng]). At integer k this is ``acquire`` at that cell.
+    Evaluated separably (x then y) over the rows/columns where the object is non-zero."""
+    ng = image_grid.shape[-1]
+    c = ng // 2
+    obj = image_grid[None] * coils                       # [J, ng, ng]
+    rows = np.flatnonzero(np.any(np.abs(image_grid) > 0, axis=1))
+    cols = np.flatnonzero(np.any(np.abs(image_grid) > 0, axis=0))
+    sub = obj[:, rows][:, :, cols]                       # [J, ry, rx]
+    k = traj.reshape(-1, 2)
+    ex = np.exp(-2j * np.pi * np.outer(k[:, 0], cols - c) / ng)    # [ns, rx]
+    ey = np.exp(-2j * np.pi * np.outer(k[:, 1], rows - c) / ng)    # [ns, ry]
+    out = np.empty((obj.shape[0], k.shape[0]), dtype=np.complex128)
+    for j in range(obj.shape[0]):
+        t = ex @ sub[j].T                                # [ns, ry]: x-transform of every row
+        out[j] = np.sum(t * ey, axis=1) / ng
+    return out.reshape(obj.shape[0], traj.shape[0], traj.shape[1]) * scale
+
+
+def radial_frame_inputs(ncoils: int, ng: int, spokes: int, turns: int, frame: int, t: float | None = None):
+    """Raw radial samples of one frame [J, spokes, ng], scaled like ``frame_inputs`` (so that the
+    fully sampled grid data have l2 norm 100)."""
+    n = ng // 2
+    img = embed(shepp_logan(n, t), ng)
+    coils = coil_maps(ncoils, ng)
+    scale = 100.0 / np.linalg.norm(acquire(img, coils, None))
+    return acquire_radial(img, coils, radial_trajectory(ng, spokes, turns, frame), scale)
