@@ -221,6 +221,30 @@ nlinv_status nlinv_debug_fft2d(nlinv_plan plan, const nlinv_c32* in, nlinv_c32* 
 long long nlinv_plan_launch_count(nlinv_plan plan);
 
 /* ---------------------------------------------------------------------------------------------
+ * GPU gridding of radial spokes ("initial interpolation of the data
+ * to the grid ... pre-processing step on the CPU", P:346 radial; reading R20). Frame f's spoke s
+ * (theta = pi (s turns + f mod turns) / (spokes turns)) carries ng readout samples at r = i - ng/2;
+ * sample (s, i) goes to the R12 cell of (r cos theta, r sin theta); a sampled cell gets the mean of
+ * its samples in ascending (s, i) order. Raw samples: c32 [count][spokes][ng] (local coils).
+ * ------------------------------------------------------------------------------------------- */
+
+/* Build the per-phase cell lists (host, integer-exact, same rule as nlinv_radial_mask) and upload
+ * them. Synchronises the device. ERR_STATE if a sample is within 1e-6 of a snap midpoint. */
+nlinv_status nlinv_plan_set_trajectory(nlinv_plan plan, int spokes, int turns);
+
+/* Grid frame `frame` (phase frame mod turns): writes y[j][cell] for every sampled cell of P_k
+ * (other cells untouched: only P_k y enters the method, R16) and sets the plan's P_k to that
+ * frame's mask. raw: device [count][spokes][ng]; y: device [count][ng][ng]. Stream-ordered.
+ * ERR_STATE before nlinv_plan_set_trajectory. */
+nlinv_status nlinv_grid_radial(nlinv_plan plan, int frame, const nlinv_c32* raw, nlinv_c32* y, void* stream);
+
+/* Real-time entry with raw radial samples (pinned host [count][spokes][ng]): H2D, GPU gridding,
+ * reconstruction with the previous frame as prior (as nlinv_stream_frame), image to image_host
+ * (host [n][n], may be NULL). Synchronises the stream before returning. */
+nlinv_status nlinv_stream_frame_radial(nlinv_plan plan, const nlinv_c32* raw_host, int frame, int newton_steps,
+                                       int cg_iters, nlinv_c32* image_host, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
  * PCA channel compression. PAPER P:241 (§3.2): "A principal component
  * analysis preprocessing step is applied before reconstruction to compress the 32 channels to
  * 8-12"; covariance C = sum_n y[n] y[n]^H (J x J), eigendecomposition, projection

@@ -6,6 +6,7 @@
 // (twiddles, w^{-1}) and the integer radial rasteriser, which are host setup.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -81,6 +82,13 @@ struct nlinv_plan_s {
   // sampled-cell index list of P_k (nlinv_mask_indices, compact ingest)
   int *midx = nullptr, *mcount = nullptr, *mnnz = nullptr;
   float2* h_samples = nullptr;
+  // radial trajectory (nlinv_plan_set_trajectory): per frame phase f mod turns, the sampled cells
+  // (ascending), CSR starts, sample ids and P_k on the device
+  int traj_spokes = 0, traj_turns = 0;
+  std::vector<int*> tr_cells, tr_start, tr_sid;
+  std::vector<uint8_t*> tr_mask;
+  std::vector<int> tr_nnz;
+  float2* h_raw = nullptr;   // staging of host raw samples (nlinv_stream_frame_radial)
   long long mnnz_host = -1;  // count of midx; -1 = index list stale (P_k changed)
   // graph cache
   GraphKey gkey;
@@ -227,6 +235,97 @@ extern "C" nlinv_status nlinv_radial_mask(int nx, int ny, int spokes, int turns,
   return NLINV_OK;
 }
 
+// ------------------------------------------------------------------ radial trajectory + GPU gridding (f2, R20)
+static nlinv_status traj_clear(nlinv_plan pl) {
+  for (int* p : pl->tr_cells) cudaFree(p);
+  for (int* p : pl->tr_start) cudaFree(p);
+  for (int* p : pl->tr_sid) cudaFree(p);
+  for (uint8_t* p : pl->tr_mask) cudaFree(p);
+  pl->tr_cells.clear();
+  pl->tr_start.clear();
+  pl->tr_sid.clear();
+  pl->tr_mask.clear();
+  pl->tr_nnz.clear();
+  pl->traj_spokes = pl->traj_turns = 0;
+  return NLINV_OK;
+}
+
+extern "C" nlinv_status nlinv_plan_set_trajectory(nlinv_plan pl, int spokes, int turns) {
+  if (!pl) return fail(pl, NLINV_ERR_ARG, "NULL plan");
+  if (spokes < 1 || turns < 1 || turns > 64) return fail(pl, NLINV_ERR_ARG, "bad spokes/turns");
+  CU(cudaDeviceSynchronize());
+  traj_clear(pl);
+  const int ng = pl->ng;
+  const size_t N = pl->N;
+  const double denom = (double)spokes * (double)turns;
+  for (int f = 0; f < turns; ++f) {
+    // cell of every sample by the R12 rule (same integer arithmetic as nlinv_radial_mask)
+    std::vector<std::pair<int, int>> cs;   // (cell, sample id), sample ids ascending
+    cs.reserve((size_t)spokes * ng);
+    for (int sp = 0; sp < spokes; ++sp) {
+      const double theta = M_PI * (double)(sp * turns + f) / denom;
+      const double ct = std::cos(theta), st = std::sin(theta);
+      for (int i = 0; i < ng; ++i) {
+        const double rr = (double)(i - ng / 2);
+        long long kx, ky;
+        if (!round_snapped(rr * ct, &kx) || !round_snapped(rr * st, &ky)) {
+          traj_clear(pl);
+          return fail(pl, NLINV_ERR_STATE, "radial sample within 1e-6 of a snap midpoint");
+        }
+        kx += ng / 2;
+        ky += ng / 2;
+        if (kx >= 0 && kx < ng && ky >= 0 && ky < ng) cs.push_back({(int)(ky * ng + kx), sp * ng + i});
+      }
+    }
+    std::stable_sort(cs.begin(), cs.end(), [](const std::pair<int, int>& a, const std::pair<int, int>& b) {
+      return a.first < b.first;
+    });
+    std::vector<int> cells, start, sid;
+    std::vector<uint8_t> m(N, 0);
+    for (size_t u = 0; u < cs.size(); ++u) {
+      if (u == 0 || cs[u].first != cs[u - 1].first) {
+        cells.push_back(cs[u].first);
+        start.push_back((int)u);
+        m[cs[u].first] = 1;
+      }
+      sid.push_back(cs[u].second);
+    }
+    start.push_back((int)cs.size());
+    int *dc = nullptr, *ds = nullptr, *di = nullptr;
+    uint8_t* dm = nullptr;
+    CU(cudaMalloc((void**)&dc, sizeof(int) * (cells.size() + 1)));
+    CU(cudaMalloc((void**)&ds, sizeof(int) * start.size()));
+    CU(cudaMalloc((void**)&di, sizeof(int) * (sid.size() + 1)));
+    CU(cudaMalloc((void**)&dm, N));
+    pl->tr_cells.push_back(dc);
+    pl->tr_start.push_back(ds);
+    pl->tr_sid.push_back(di);
+    pl->tr_mask.push_back(dm);
+    pl->tr_nnz.push_back((int)cells.size());
+    if (!cells.empty()) CU(cudaMemcpy(dc, cells.data(), sizeof(int) * cells.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ds, start.data(), sizeof(int) * start.size(), cudaMemcpyHostToDevice));
+    if (!sid.empty()) CU(cudaMemcpy(di, sid.data(), sizeof(int) * sid.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(dm, m.data(), N, cudaMemcpyHostToDevice));
+  }
+  pl->traj_spokes = spokes;
+  pl->traj_turns = turns;
+  return NLINV_OK;
+}
+
+extern "C" nlinv_status nlinv_grid_radial(nlinv_plan pl, int frame, const nlinv_c32* raw, nlinv_c32* y, void* stream) {
+  if (!pl || !raw || !y || frame < 0) return fail(pl, NLINV_ERR_ARG, "bad argument to nlinv_grid_radial");
+  if (pl->traj_turns == 0) return fail(pl, NLINV_ERR_STATE, "nlinv_grid_radial before nlinv_plan_set_trajectory");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int f = frame % pl->traj_turns;
+  const int nraw = pl->traj_spokes * pl->ng;
+  CU(cudaMemcpyAsync(pl->mask, pl->tr_mask[f], pl->N, cudaMemcpyDeviceToDevice, s));
+  pl->mnnz_host = -1;
+  CU(launch_grid_radial(reinterpret_cast<const float2*>(raw), pl->J, nraw, pl->tr_cells[f], pl->tr_start[f],
+                        pl->tr_sid[f], pl->tr_nnz[f], pl->N, reinterpret_cast<float2*>(y), s));
+  pl->launches += 1;
+  return NLINV_OK;
+}
+
 extern "C" nlinv_status nlinv_coil_partition(int ncoils, int world, int rank, int* first, int* count) {
   nlinv_plan pl = nullptr;
   if (!first || !count) return fail(pl, NLINV_ERR_ARG, "NULL argument");
@@ -240,6 +339,11 @@ extern "C" nlinv_status nlinv_coil_partition(int ncoils, int world, int rank, in
 
 // ------------------------------------------------------------------ plan
 static void plan_free(nlinv_plan pl) {
+  for (int* p : pl->tr_cells) cudaFree(p);
+  for (int* p : pl->tr_start) cudaFree(p);
+  for (int* p : pl->tr_sid) cudaFree(p);
+  for (uint8_t* p : pl->tr_mask) cudaFree(p);
+  cudaFree(pl->h_raw);
   if (!pl) return;
   void* ptrs[] = {pl->tw, pl->winv, pl->mask, pl->xref, pl->dx, pl->r, pl->p, pl->Ap, pl->tA, pl->tB,
                   pl->c_omega, pl->rho_omega, pl->S_all, pl->S, pl->S_sum, pl->rss_all, pl->rss, pl->rss_sum,
@@ -1174,6 +1278,33 @@ extern "C" nlinv_status nlinv_stream_frame_compact(nlinv_plan pl, const nlinv_c3
   CU(cudaMemcpyAsync(pl->h_samples, samples_host, sizeof(float2) * (size_t)nnz * pl->J, cudaMemcpyHostToDevice, s));
   CU(launch_scatter_samples(pl->h_samples, pl->midx, pl->mnnz, nnz, pl->J, N, pl->h_frame, s));
   pl->launches += 1;
+  st = nlinv_reconstruct(pl, (const nlinv_c32*)pl->h_frame, pl->stream_started ? (const nlinv_c32*)pl->h_x : nullptr,
+                         newton_steps, cg_iters, (nlinv_c32*)pl->h_x, image_host ? (nlinv_c32*)pl->h_img : nullptr,
+                         stream);
+  if (st != NLINV_OK) return st;
+  pl->stream_started = true;
+  if (image_host) CU(cudaMemcpyAsync(image_host, pl->h_img, sizeof(float2) * pl->Q, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return NLINV_OK;
+}
+
+extern "C" nlinv_status nlinv_stream_frame_radial(nlinv_plan pl, const nlinv_c32* raw_host, int frame, int newton_steps,
+                                                  int cg_iters, nlinv_c32* image_host, void* stream) {
+  if (!pl || !raw_host || frame < 0) return fail(pl, NLINV_ERR_ARG, "bad argument");
+  if (pl->traj_turns == 0) return fail(pl, NLINV_ERR_STATE, "nlinv_stream_frame_radial before nlinv_plan_set_trajectory");
+  const size_t N = pl->N, tot = N * (1 + pl->J);
+  const size_t nraw = (size_t)pl->traj_spokes * pl->ng;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!pl->h_frame) {
+    CU(cudaMalloc((void**)&pl->h_frame, sizeof(float2) * N * pl->J));
+    CU(cudaMemset(pl->h_frame, 0, sizeof(float2) * N * pl->J));
+    CU(cudaMalloc((void**)&pl->h_x, sizeof(float2) * tot));
+    CU(cudaMalloc((void**)&pl->h_img, sizeof(float2) * pl->Q));
+  }
+  if (!pl->h_raw) CU(cudaMalloc((void**)&pl->h_raw, sizeof(float2) * nraw * pl->J));
+  CU(cudaMemcpyAsync(pl->h_raw, raw_host, sizeof(float2) * nraw * pl->J, cudaMemcpyHostToDevice, s));
+  nlinv_status st = nlinv_grid_radial(pl, frame, (const nlinv_c32*)pl->h_raw, (nlinv_c32*)pl->h_frame, stream);
+  if (st != NLINV_OK) return st;
   st = nlinv_reconstruct(pl, (const nlinv_c32*)pl->h_frame, pl->stream_started ? (const nlinv_c32*)pl->h_x : nullptr,
                          newton_steps, cg_iters, (nlinv_c32*)pl->h_x, image_host ? (nlinv_c32*)pl->h_img : nullptr,
                          stream);

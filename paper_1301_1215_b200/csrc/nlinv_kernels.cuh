@@ -162,6 +162,8 @@ cudaError_t launch_frame(int ng, const FrameArgs& f, cudaStream_t s);
 bool frame_supported(int ng);
 cudaError_t launch_mask_compact(const uint8_t* mask, int N, int* counts, int* idx, int* nnz, cudaStream_t s);
 int mask_count_blocks(int N);
+cudaError_t launch_grid_radial(const float2* raw, int J, int nraw, const int* cells, const int* start, const int* sid,
+                               int nnz, size_t N, float2* y, cudaStream_t s);
 cudaError_t launch_scatter_samples(const float2* samples, const int* idx, const int* nnz, int nnz_cap, int J,
                                    size_t N, float2* y, cudaStream_t s);
 bool col_fusable(int ng, int J);

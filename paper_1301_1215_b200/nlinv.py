@@ -74,6 +74,9 @@ _SIGS = {
     "nlinv_plan_phase_times": (c_int, [c_void_p, c_int, c_void_p, c_int, ctypes.POINTER(c_int)]),
     "nlinv_plan_trace": (c_int, [c_void_p, c_int, c_void_p, c_int]),
     "nlinv_plan_profile_json": (c_int, [c_void_p, ctypes.c_char_p, ctypes.c_size_t]),
+    "nlinv_plan_set_trajectory": (c_int, [c_void_p, c_int, c_int]),
+    "nlinv_grid_radial": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
+    "nlinv_stream_frame_radial": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p]),
     "nlinv_pca_create": (c_int, [c_int, c_int, ctypes.POINTER(c_void_p)]),
     "nlinv_pca_destroy": (c_int, [c_void_p]),
     "nlinv_pca_fit": (c_int, [c_void_p, c_void_p, c_ll, c_void_p]),
@@ -298,6 +301,41 @@ class Plan:
             ip = ctypes.c_void_p(image_out.data_ptr())
         _check(_lib.nlinv_stream_frame_compact(self._h, ctypes.c_void_p(samples.data_ptr()), int(samples.shape[1]), mp,
                                                int(newton_steps), int(cg_iters), ip, _stream_ptr(stream)), self._h)
+        return image_out
+
+    def set_trajectory(self, spokes: int, turns: int):
+        """Radial trajectory for GPU gridding (R12 cells, R20 mean per cell)."""
+        self.spokes, self.turns = int(spokes), int(turns)
+        _check(_lib.nlinv_plan_set_trajectory(self._h, self.spokes, self.turns), self._h)
+
+    def grid_radial(self, frame: int, raw, y=None, stream=None):
+        """Grid raw radial samples (CUDA complex64 [count, spokes, ng]) of frame `frame` into y
+        (CUDA complex64 [count, ng, ng]); also sets the plan's P_k to that frame's mask."""
+        import torch
+        shape = (self.count, self.spokes, self.ng)
+        if not (raw.is_cuda and raw.dtype == torch.complex64 and tuple(raw.shape) == shape and raw.is_contiguous()):
+            raise ValueError(f"raw must be a contiguous CUDA complex64 tensor {shape}")
+        if y is None:
+            y = torch.zeros(self.y_shape, dtype=torch.complex64, device=raw.device)
+        yp = self._t(y, self.y_shape, "y")
+        _check(_lib.nlinv_grid_radial(self._h, int(frame), c_void_p(raw.data_ptr()), yp, _stream_ptr(stream)),
+               self._h)
+        return y
+
+    def stream_frame_radial(self, raw, frame: int, newton_steps=7, cg_iters=10, image_out=None, stream=None):
+        """Real-time entry with raw radial samples: pinned host complex64 [count, spokes, ng] in,
+        host image out (GPU gridding + reconstruction with the previous frame as prior)."""
+        import torch
+        shape = (self.count, self.spokes, self.ng)
+        if raw.is_cuda or raw.dtype != torch.complex64 or tuple(raw.shape) != shape or not raw.is_contiguous():
+            raise ValueError(f"raw must be a contiguous CPU complex64 tensor {shape}")
+        ip = None
+        if image_out is not None:
+            if image_out.is_cuda or image_out.dtype != torch.complex64 or tuple(image_out.shape) != self.image_shape:
+                raise ValueError("image_out must be a CPU complex64 tensor [n, n]")
+            ip = ctypes.c_void_p(image_out.data_ptr())
+        _check(_lib.nlinv_stream_frame_radial(self._h, ctypes.c_void_p(raw.data_ptr()), int(frame), int(newton_steps),
+                                              int(cg_iters), ip, _stream_ptr(stream)), self._h)
         return image_out
 
     def stream_reset(self):
