@@ -1036,7 +1036,7 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) k5cg_kernel(ColA
 // Groups are independent (each inside one warp); no CTA-wide barrier is used.
 template <int L, int MODE>
 __device__ __forceinline__ void row_task(const RowArgs& a, int pair0, const float2* tw, float2* xbase,
-                                         bool tw_async = false) {
+                                         bool tw_async = false, float2* cst = nullptr) {
   using C = Cfg<L>;
   using S = Sched<L>;
   constexpr int T = C::T, E = C::E;
@@ -1055,6 +1055,33 @@ __device__ __forceinline__ void row_task(const RowArgs& a, int pair0, const floa
       for (int i = t; i < n; i += T) a.rho_omega[(size_t)yy * n + i] = a.xrho[(size_t)row * L + q + i];
   }
   float2 v[E];
+  // K2 with staging (row_kernel, cst != nullptr): c_j|Omega and rho|Omega of this row do not depend
+  // on the previous pass (they are fixed for the Newton step), so they are copied into shared
+  // memory BEFORE griddepcontrol.wait and land while the previous pass drains; p_rho (written by
+  // the previous pass) follows after the wait. 16-byte cp.async, read back after tw_wait.
+  float2* gst = nullptr;
+  if constexpr (MODE == RK_K2) {
+    if (cst != nullptr) {
+      gst = cst + (size_t)g * 3 * n;
+      const int jj = active ? j : 0, y2 = active ? yy : 0;
+      const float2* srcs[2] = {a.c_omega + jj * Q + (size_t)y2 * n, a.rho_omega + (size_t)y2 * n};
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+        for (int i = t; i < n / 2; i += T) {
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(gst + b * n + 2 * i);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(srcs[b] + 2 * i));
+        }
+      asm volatile("cp.async.commit_group;\n" ::);
+      pdl_wait();
+      pdl_trigger();
+      const float2* pr_src = a.prho + (size_t)(q + y2) * L + q;
+      for (int i = t; i < n / 2; i += T) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(gst + 2 * n + 2 * i);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(pr_src + 2 * i));
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+    }
+  }
   // Unconditional loads: an inactive group (tail of the last CTA) transforms a valid row it never
   // stores. A per-element "if (active)" makes the compiler put each load and its first use in one
   // branch region, which serialises the E load latencies.
@@ -1091,7 +1118,11 @@ __device__ __forceinline__ void row_task(const RowArgs& a, int pair0, const floa
     for (int e = 0; e < E; ++e) {
       if (out_is_omega<L>(e)) {
         const int k = S::out_idx(t, e);
-        if (active) {
+        if (gst != nullptr) {   // staged rows (valid for inactive groups too: row 0 of coil 0)
+          cv[u] = gst[k - q];
+          rv[u] = gst[n + (k - q)];
+          pr[u] = gst[2 * n + (k - q)];
+        } else if (active) {
           cv[u] = a.c_omega[j * Q + (size_t)yy * n + (k - q)];
           rv[u] = a.rho_omega[(size_t)yy * n + (k - q)];
           pr[u] = a.prho[(size_t)row * L + k];
@@ -1163,7 +1194,7 @@ __device__ __forceinline__ void row_task(const RowArgs& a, int pair0, const floa
 // sum_j conj(c_j) u_j (Table 1 "sum c_j") is formed in shared memory in ascending coil order.
 template <int L>
 __device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, int jlo, int jhi, int plane, const float2* tw,
-                                            float2* xbase, float2* accs, bool tw_async = false) {
+                                            float2* xbase, float2* accs, bool tw_async = false, bool pre_wait = false) {
   using C = Cfg<L>;
   using S = Sched<L>;
   constexpr int T = C::T, E = C::E;
@@ -1181,25 +1212,30 @@ __device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, int jlo, i
     int u = 0;
 #pragma unroll
     for (int e = 0; e < E; ++e)
-      if (out_is_omega<L>(e)) rv[u++] = a.rho_omega[(size_t)yy * n + (S::out_idx(t, e) - q)];
+      if (out_is_omega<L>(e)) rv[u++] = __ldcg(a.rho_omega + (size_t)yy * n + (S::out_idx(t, e) - q));
   }
   for (int j0 = jlo; j0 < jhi; j0 += GPC) {
     const int j = j0 + g;
     const bool active = j < jhi;
     float2 v[E], cv[E / 2];
-    {  // unconditional loads (see row_task); an inactive group's result is masked below
-      const float2* src = a.in + (size_t)(active ? j : jlo) * H + (size_t)yy * L;
-#pragma unroll
-      for (int e = 0; e < E; ++e) v[e] = cneg_if(src[S::in_idx(t, e)], S::in_idx(t, e) & 1);
-    }
-    {
+    {  // c_j|Omega is fixed for the Newton step: loaded before griddepcontrol.wait (pre_wait)
       int u = 0;
 #pragma unroll
       for (int e = 0; e < E; ++e)
         if (out_is_omega<L>(e)) {
-          cv[u] = active ? a.c_omega[j * Q + (size_t)yy * n + (S::out_idx(t, e) - q)] : make_float2(0.f, 0.f);
+          // ld.global.cg: L2 is the coherence point for data of an earlier grid read before the wait
+          cv[u] = active ? __ldcg(a.c_omega + j * Q + (size_t)yy * n + (S::out_idx(t, e) - q)) : make_float2(0.f, 0.f);
           ++u;
         }
+    }
+    if (pre_wait && j0 == jlo) {
+      pdl_wait();
+      pdl_trigger();
+    }
+    {  // unconditional loads (see row_task); an inactive group's result is masked below
+      const float2* src = a.in + (size_t)(active ? j : jlo) * H + (size_t)yy * L;
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = cneg_if(src[S::in_idx(t, e)], S::in_idx(t, e) & 1);
     }
     if (tw_async && j0 == jlo) tw_wait();
     fft<L, +1>(v, t, tw, buf, SyncWarp{});
@@ -1266,6 +1302,7 @@ struct RowGeo {
   static constexpr int THREADS = 256;
   static constexpr int GPC = THREADS / T;  // (coil, row) pairs per CTA
   static constexpr size_t SMEM = sizeof(float2) * (size_t)L * (GPC + 1) + sizeof(float2) * (L / 2);
+  static constexpr size_t SMEM_K2 = sizeof(float2) * ((size_t)L * (GPC + 1) + (size_t)GPC * 3 * (L / 2));
 };
 
 template <int L, int MODE>
@@ -1274,15 +1311,20 @@ __global__ void __launch_bounds__(256, NLV_MINB) row_kernel(RowArgs a, const flo
   float2* tw = reinterpret_cast<float2*>(smem_raw);
   float2* xb = tw + L;
   tw_copy_async(tw, twg, L);
-  pdl_wait();
-  pdl_trigger();
   if constexpr (MODE == RK_K4) {
-    // CTA = (Omega row, chunk of a.kchunk coils); chunk c writes coil-sum plane c
+    // CTA = (Omega row, chunk of a.kchunk coils); chunk c writes coil-sum plane c. rho|Omega and
+    // c_j|Omega (fixed for the Newton step) are read before griddepcontrol.wait
     const int jlo = blockIdx.y * a.kchunk, jhi = min(a.J, jlo + a.kchunk);
-    row_task_k4<L>(a, blockIdx.x, jlo, jhi, blockIdx.y, tw, xb, xb + (size_t)L * (blockDim.x / Cfg<L>::T), true);
-  }
-  else
+    row_task_k4<L>(a, blockIdx.x, jlo, jhi, blockIdx.y, tw, xb, xb + (size_t)L * (blockDim.x / Cfg<L>::T), true, true);
+  } else if constexpr (MODE == RK_K2) {
+    // per-group staging of c_j|Omega, rho|Omega, p_rho|Omega after the exchange buffers (RowGeo::SMEM_K2)
+    const int gpc = blockDim.x / Cfg<L>::T;
+    row_task<L, MODE>(a, blockIdx.x * gpc, tw, xb, true, xb + (size_t)L * gpc);
+  } else {
+    pdl_wait();
+    pdl_trigger();
     row_task<L, MODE>(a, blockIdx.x * (blockDim.x / Cfg<L>::T), tw, xb, true);
+  }
 }
 
 // ------------------------------------------------------------------ persistent frame kernel
@@ -1945,6 +1987,12 @@ static cudaError_t launch_row_t(const RowArgs& a0, const float2* tw, cudaStream_
   } else {
     const int gpc = row_pairs_per_cta<L>();
     const int grid = (a0.J * (L / 2) + gpc - 1) / gpc;
+    if constexpr (MODE == RK_K2) {
+      const size_t sm2 = sizeof(float2) * ((size_t)L * (gpc + 1) + (size_t)gpc * 3 * (L / 2));
+      if (sm2 > smem && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) != cudaSuccess)
+        return e;
+      return launch_k(kern, dim3(grid), dim3(gpc * Cfg<L>::T), sm2 > smem ? sm2 : smem, s, a0, tw);
+    }
     return launch_k(kern, dim3(grid), dim3(gpc * Cfg<L>::T), smem, s, a0, tw);
   }
 }
