@@ -756,6 +756,9 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   const unsigned nb = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
   ColBuf<CW> buf{xb, c};
 
+  // r (dx in the last iteration) was written by the previous CG iteration's pass, which completed
+  // before the passes in between could run: the L2-only (cp.async.cg) prefetch is issued before
+  // griddepcontrol.wait and overlaps the drain of the previous pass
   bool pf_on = false;
   if (!last) {
     tile_prefetch<L, CW>(pf, a.r + j * N, tile * CW);
@@ -764,6 +767,8 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
     tile_prefetch<L, CW>(pf, a.dx + j * N, tile * CW);
     pf_on = true;
   }
+  pdl_wait();
+  pdl_trigger();
 
   // prologue: T4 (Omega rows only; the others are zero)
   float2 v[E];
@@ -1024,9 +1029,7 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) k5cg_kernel(ColA
   float2* pf = reinterpret_cast<float2*>(red + 128);
   trace_stamp(a.trace, 0);
   tw_copy_async(tw, twg, L);
-  pdl_wait();
-  pdl_trigger();
-  k5cg_task<L>(a, tw, xb, pf, red);
+  k5cg_task<L>(a, tw, xb, pf, red);   // griddepcontrol.wait inside, after the r prefetch
   trace_stamp(a.trace, 5);
   trace_stamp(a.trace, 6);
 }
@@ -1890,18 +1893,23 @@ static cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
 }
 
 template <typename... KArgs, typename... Act>
-static cudaError_t launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+static cudaError_t launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
                                Act&&... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  // cooperative (grid barriers); optionally with programmatic dependent launch, so the pass is
+  // scheduled while the previous one drains (its CTAs reach a grid barrier only after
+  // griddepcontrol.wait, i.e. after the previous pass has released every SM)
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = (pdl && pdl_enabled()) ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
 }
 
@@ -1938,7 +1946,7 @@ static cudaError_t launch_k5cg_t(const ColArgs& a, const float2* tw, cudaStream_
   const size_t smem = ColGeo<L>::SMEM_PF;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_coop(kern, dim3(L / ColGeo<L>::CW, a.J), dim3(ColGeo<L>::THREADS), smem, s, a, tw);
+  return launch_coop(kern, dim3(L / ColGeo<L>::CW, a.J), dim3(ColGeo<L>::THREADS), smem, s, true, a, tw);
 }
 
 template <int L, int MODE>
@@ -1950,7 +1958,7 @@ static cudaError_t launch_col_t(const ColArgs& a, const float2* tw, cudaStream_t
   const int gy = ((MODE == CK_IFFT_W_CG || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ) &&
                   !a.rho_spread) ? a.J + 1 : a.J;
   dim3 grid(L / ColGeo<L>::CW, gy);
-  if (MODE == CK_FFT_W_NORMAL && a.fuse_update) return launch_coop(kern, grid, dim3(ColGeo<L>::THREADS), smem, s, a, tw);
+  if (MODE == CK_FFT_W_NORMAL && a.fuse_update) return launch_coop(kern, grid, dim3(ColGeo<L>::THREADS), smem, s, false, a, tw);
   return launch_k(kern, grid, dim3(ColGeo<L>::THREADS), smem, s, a, tw);
 }
 
