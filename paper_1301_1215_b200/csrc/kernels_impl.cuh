@@ -242,7 +242,7 @@ __device__ __forceinline__ void trace_stamp(unsigned long long* tr, int k) {
 template <int L, int MODE>
 __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, const float2* tw, float2* xb,
                                          double& acc_rho, double& acc, double* acc3, int rlo = 0, int rhi = L,
-                                         bool tw_async = false) {
+                                         bool tw_async = false, const uint32_t* pre_mbits = nullptr) {
   using C = Cfg<L>;
   using S = Sched<L>;
   constexpr int T = C::T, E = C::E, CW = ColGeo<L>::CW;
@@ -410,8 +410,12 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
   // mask bits of this thread's k-space rows, fetched before the transform (latency hidden)
   uint32_t mbits = 0;
   if constexpr (MODE == CK_PSF || MODE == CK_RESADJ || MODE == CK_FWDP) {
+    if (pre_mbits != nullptr) {
+      mbits = *pre_mbits;
+    } else {
 #pragma unroll
-    for (int e = 0; e < E; ++e) mbits |= (a.mask[(size_t)S::out_idx(t, e) * L + x] ? 1u : 0u) << e;
+      for (int e = 0; e < E; ++e) mbits |= (a.mask[(size_t)S::out_idx(t, e) * L + x] ? 1u : 0u) << e;
+    }
   }
 
   if (tw_async) tw_wait();
@@ -695,6 +699,15 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColAr
   double* red = reinterpret_cast<double*>(xb + (size_t)L * CW);
   trace_stamp(a.trace, 0);
   tw_copy_async(tw, twg, L);
+  // K3: P_k is fixed for the frame (set before its first pass): its bits are read (L2-coherent
+  // ld.global.cg) before griddepcontrol.wait
+  uint32_t mb = 0;
+  if constexpr (MODE == CK_PSF) {
+    using S = Sched<L>;
+    const int c = threadIdx.x % CW, t = threadIdx.x / CW, x = blockIdx.x * CW + c;
+#pragma unroll
+    for (int e = 0; e < Cfg<L>::E; ++e) mb |= (__ldcg(a.mask + (size_t)S::out_idx(t, e) * L + x) ? 1u : 0u) << e;
+  }
   pdl_wait();
   pdl_trigger();
   if constexpr (MODE == CK_IFFT_W_CG) {
@@ -706,7 +719,7 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColAr
   const bool has_rho = (MODE == CK_IFFT_W_CG || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ);
   const int j = (has_rho && !a.rho_spread) ? (blockIdx.y == 0 ? a.J : (int)blockIdx.y - 1) : (int)blockIdx.y;
   double acc3[4] = {0.0, 0.0, 0.0, 0.0};
-  col_task<L, MODE>(a, blockIdx.x, j, tw, xb, acc_rho, acc, acc3, 0, L, true);
+  col_task<L, MODE>(a, blockIdx.x, j, tw, xb, acc_rho, acc, acc3, 0, L, true, MODE == CK_PSF ? &mb : nullptr);
   trace_stamp(a.trace, 5);
   if constexpr (MODE == CK_RESADJ || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_NORMAL) {
     if (MODE == CK_FFT_W_NORMAL && a.fuse_update) {
