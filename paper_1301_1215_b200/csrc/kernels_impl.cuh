@@ -1897,11 +1897,15 @@ static cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (access_window(&attr[1].val.accessPolicyWindow)) {
+    attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+    cfg.numAttrs = 2;
+  }
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
 }
 
@@ -1916,13 +1920,17 @@ static cudaError_t launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, si
   // cooperative (grid barriers); optionally with programmatic dependent launch, so the pass is
   // scheduled while the previous one drains (its CTAs reach a grid barrier only after
   // griddepcontrol.wait, i.e. after the previous pass has released every SM)
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = (pdl && pdl_enabled()) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
+  if (access_window(&attr[2].val.accessPolicyWindow)) {
+    attr[2].id = cudaLaunchAttributeAccessPolicyWindow;
+    cfg.numAttrs = 3;
+  }
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
 }
 

@@ -89,6 +89,7 @@ struct nlinv_plan_s {
   std::vector<uint8_t*> tr_mask;
   std::vector<int> tr_nnz;
   float2* h_raw = nullptr;   // staging of host raw samples (nlinv_stream_frame_radial)
+  void* slab = nullptr;      // one allocation for the per-iteration working set (L2 access window)
   long long mnnz_host = -1;  // count of midx; -1 = index list stale (P_k changed)
   // graph cache
   GraphKey gkey;
@@ -339,12 +340,17 @@ extern "C" nlinv_status nlinv_coil_partition(int ncoils, int world, int rank, in
 
 // ------------------------------------------------------------------ plan
 static void plan_free(nlinv_plan pl) {
+  if (!pl) return;
   for (int* p : pl->tr_cells) cudaFree(p);
   for (int* p : pl->tr_start) cudaFree(p);
   for (int* p : pl->tr_sid) cudaFree(p);
   for (uint8_t* p : pl->tr_mask) cudaFree(p);
   cudaFree(pl->h_raw);
-  if (!pl) return;
+  if (pl->slab) {   // tA, tB, dx, r, p, c_omega live in the L2-persisting slab
+    clear_access_window(pl->slab);
+    cudaFree(pl->slab);
+    pl->tA = pl->tB = pl->dx = pl->r = pl->p = pl->c_omega = nullptr;
+  }
   void* ptrs[] = {pl->tw, pl->winv, pl->mask, pl->xref, pl->dx, pl->r, pl->p, pl->Ap, pl->tA, pl->tB,
                   pl->c_omega, pl->rho_omega, pl->S_all, pl->S, pl->S_sum, pl->rss_all, pl->rss, pl->rss_sum,
                   pl->fred, pl->fbar, pl->fdone, pl->ftred, pl->tstamp, pl->kbar, pl->kpart, pl->scal, pl->partials,
@@ -409,13 +415,34 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
   ok &= alloc((void**)&pl->winv, sizeof(float) * N);
   ok &= alloc((void**)&pl->mask, N);
   ok &= alloc((void**)&pl->xref, sizeof(float2) * N * nb);
-  ok &= alloc((void**)&pl->dx, sizeof(float2) * N * nb);
-  ok &= alloc((void**)&pl->r, sizeof(float2) * N * nb);
-  ok &= alloc((void**)&pl->p, sizeof(float2) * N * nb);
+  // The per-CG-iteration working set (T intermediates, c|Omega, r, p, dx: ~65 MB at C2) is one
+  // slab. NLINV_L2PERSIST=1 marks it L2-persisting (access-policy window on every launch); measured
+  // on B200 at C2 that is within noise (+0.6 %: the passes are not DRAM bound), so it is off by
+  // default and the bench's per-frame L2 flush really flushes everything.
+  {
+    const char* lp = std::getenv("NLINV_L2PERSIST");
+    const bool persist = (lp && lp[0] == '1');
+    const size_t b_t = sizeof(float2) * pl->H * pl->J, b_v = sizeof(float2) * N * nb, b_c = sizeof(float2) * pl->Q * pl->J;
+    const size_t tot_b = 2 * b_t + 3 * b_v + b_c;
+    if (alloc(&pl->slab, tot_b)) {
+      char* b = (char*)pl->slab;
+      pl->tA = (float2*)b;
+      pl->tB = (float2*)(b + b_t);
+      pl->r = (float2*)(b + 2 * b_t);
+      pl->p = (float2*)(b + 2 * b_t + b_v);
+      pl->dx = (float2*)(b + 2 * b_t + 2 * b_v);
+      pl->c_omega = (float2*)(b + 2 * b_t + 3 * b_v);
+      if (persist) set_access_window(pl->slab, tot_b);
+    } else {
+      ok &= alloc((void**)&pl->dx, b_v);
+      ok &= alloc((void**)&pl->r, b_v);
+      ok &= alloc((void**)&pl->p, b_v);
+      ok &= alloc((void**)&pl->tA, b_t);
+      ok &= alloc((void**)&pl->tB, b_t);
+      ok &= alloc((void**)&pl->c_omega, b_c);
+    }
+  }
   ok &= alloc((void**)&pl->Ap, sizeof(float2) * N * nb);
-  ok &= alloc((void**)&pl->tA, sizeof(float2) * pl->H * pl->J);
-  ok &= alloc((void**)&pl->tB, sizeof(float2) * pl->H * pl->J);
-  ok &= alloc((void**)&pl->c_omega, sizeof(float2) * pl->Q * pl->J);
   ok &= alloc((void**)&pl->rho_omega, sizeof(float2) * pl->Q);
   ok &= alloc((void**)&pl->S, sizeof(float2) * pl->Q);
   ok &= alloc((void**)&pl->S_all, sizeof(float2) * pl->Q * pl->J);

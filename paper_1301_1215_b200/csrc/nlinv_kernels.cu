@@ -29,6 +29,37 @@ int k4_planes(int ng, int J) {
   return J;
 }
 
+namespace {
+cudaAccessPolicyWindow g_apw{};
+bool g_apw_on = false;
+}  // namespace
+void set_access_window(void* base, size_t bytes) {
+  int dev = 0, maxp = 0, maxw = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+  cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+  if (maxp <= 0 || maxw <= 0) return;
+  size_t win = bytes < (size_t)maxw ? bytes : (size_t)maxw;
+  size_t carve = win < (size_t)maxp ? win : (size_t)maxp;
+  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  g_apw.base_ptr = base;
+  g_apw.num_bytes = win;
+  g_apw.hitRatio = (float)((double)carve / (double)win);
+  g_apw.hitProp = cudaAccessPropertyPersisting;
+  g_apw.missProp = cudaAccessPropertyStreaming;
+  g_apw_on = true;
+}
+void clear_access_window(void* base) {
+  if (g_apw_on && g_apw.base_ptr == base) g_apw_on = false;
+}
+bool access_window(cudaAccessPolicyWindow* w) {
+  if (!g_apw_on) return false;
+  *w = g_apw;
+  return true;
+}
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("NLINV_PDL");

@@ -155,7 +155,12 @@ cudaError_t launch_image(int ng, const float2* rho_omega, const float* rss, int 
 cudaError_t launch_fft2d(int ng, const float2* in, float2* out, int batch, int inverse, const float2* tw,
                          float2* tmp, cudaStream_t s);
 bool supported_ng(int ng);
-bool pdl_enabled();      // programmatic dependent launch between passes (NLINV_PDL=0 disables)
+bool pdl_enabled();
+// L2 access-policy window (persisting) attached to every launch of the library; set by the plan
+// that owns the working-set slab (the most recent one), cleared when it is freed
+void set_access_window(void* base, size_t bytes);
+void clear_access_window(void* base);
+bool access_window(cudaAccessPolicyWindow* w);      // programmatic dependent launch between passes (NLINV_PDL=0 disables)
 int col_tiles(int ng);  // column-kernel CTAs per coil
 cudaError_t launch_init_x(float2* x, long long nrho, long long ntot, cudaStream_t s);
 cudaError_t launch_frame(int ng, const FrameArgs& f, cudaStream_t s);
