@@ -101,6 +101,24 @@ struct DFT<4, DIR> {
   }
 };
 
+// a * e^{DIR 2 pi i k48 / 48} for a compile-time k48: quarter turns are exact sign/swap moves
+// (a multiply by the literal 0 cannot be folded under IEEE rules, so cmul would waste 4 FP ops),
+// eighth turns use (x -+ y) sqrt(1/2) (2 FADD + 2 FMUL), the rest a full complex multiply.
+template <int DIR>
+__device__ __forceinline__ float2 mul_root48(float2 a, int k48) {
+  const int k = ((k48 % 48) + 48) % 48;
+  if (k == 0) return a;
+  if (k == 24) return make_float2(-a.x, -a.y);
+  if (k == 12) return mul_dir_i<DIR>(a);                       // e^{DIR i pi/2} = DIR i
+  if (k == 36) return mul_dir_i<-DIR>(a);
+  constexpr float h = 0.707106781186547524f;
+  if (k == 6) return DIR < 0 ? make_float2((a.x + a.y) * h, (a.y - a.x) * h) : make_float2((a.x - a.y) * h, (a.x + a.y) * h);
+  if (k == 18) return DIR < 0 ? make_float2((a.y - a.x) * h, -(a.x + a.y) * h) : make_float2(-(a.x + a.y) * h, (a.x - a.y) * h);
+  if (k == 30) return DIR < 0 ? make_float2(-(a.x + a.y) * h, (a.x - a.y) * h) : make_float2((a.y - a.x) * h, -(a.x + a.y) * h);
+  if (k == 42) return DIR < 0 ? make_float2((a.x - a.y) * h, (a.x + a.y) * h) : make_float2((a.x + a.y) * h, (a.y - a.x) * h);
+  return cmul(a, unit_root48<DIR>(k));
+}
+
 // Cooley-Tukey split R = R1*R2 entirely in registers: n = R2 n1 + n2, k = k1 + R1 k2.
 template <int R1, int R2, int DIR>
 __device__ __forceinline__ void dft_split(float2* a) {
@@ -115,7 +133,7 @@ __device__ __forceinline__ void dft_split(float2* a) {
 #pragma unroll
     for (int k1 = 0; k1 < R1; ++k1) {
       const int m = (n2 * k1) % R;
-      b[n2 * R1 + k1] = (m == 0) ? t[k1] : cmul(t[k1], unit_root48<DIR>(m * (48 / R)));
+      b[n2 * R1 + k1] = mul_root48<DIR>(t[k1], m * (48 / R));
     }
   }
 #pragma unroll
