@@ -68,6 +68,7 @@ struct nlinv_plan_s {
   bool gexec_valid_reset = false;
   int trace_mode = -1;                    // debug: column mode whose CTA timelines are recorded
   bool rho_spread = true;                 // rho block in stripes over the coil tiles (NLINV_RHO_SPREAD=0: own CTAs)
+  bool multi = false;                     // collective code path (world > 1 or NLINV_FORCE_NCCL=1)
   bool fuse_k5 = false;                   // K5 + r update as one cooperative pass (world == 1, fits one wave)
   bool fuse_k1 = false;                   // ... also K1 of the next iteration / the Newton update
   bool k5cg1 = false;                     // fused K5 + CG + K1 with a single grid barrier (k5cg_kernel)
@@ -400,6 +401,18 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
   pl->Q = (size_t)pl->n * pl->n;
   pl->rank = prm.rank;
   pl->world = prm.world;
+  {
+    // multi-GPU code path (coil-sum and scalar all-reduces through NCCL, unfused CG): world > 1,
+    // or NLINV_FORCE_NCCL=1 on one GPU (a one-rank communicator: the collective plumbing is then
+    // exercised and parity-tested on a single device)
+    const char* fn = std::getenv("NLINV_FORCE_NCCL");
+#ifdef NLINV_WITH_NCCL
+    pl->multi = prm.world > 1 || (fn && fn[0] == '1');
+#else
+    pl->multi = false;
+    (void)fn;
+#endif
+  }
   nlinv_coil_partition(ncoils, prm.world, prm.rank, &pl->first, &pl->count);
   pl->J = pl->count;
   if ((long long)col_tiles(nx) * (pl->J + 1) > kMaxRedBlocks) {
@@ -447,7 +460,7 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
   ok &= alloc((void**)&pl->S, sizeof(float2) * pl->Q);
   ok &= alloc((void**)&pl->S_all, sizeof(float2) * pl->Q * pl->J);
   ok &= alloc((void**)&pl->rss_all, sizeof(float) * pl->Q * pl->J);
-  if (pl->world > 1) {
+  if (pl->multi) {
     ok &= alloc((void**)&pl->rss, sizeof(float) * pl->Q);
     ok &= alloc((void**)&pl->S_sum, sizeof(float2) * pl->Q);
     ok &= alloc((void**)&pl->rss_sum, sizeof(float) * pl->Q);
@@ -458,7 +471,7 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
     const char* rs = std::getenv("NLINV_RHO_SPREAD");
     pl->rho_spread = !(rs && rs[0] == '0');
     const char* fk = std::getenv("NLINV_FUSE_K5");
-    pl->fuse_k5 = pl->rho_spread && pl->world == 1 && !(fk && fk[0] == '0') && col_fusable(nx, pl->J);
+    pl->fuse_k5 = pl->rho_spread && !pl->multi && !(fk && fk[0] == '0') && col_fusable(nx, pl->J);
     if (pl->fuse_k5) {
       ok &= alloc((void**)&pl->kbar, sizeof(unsigned) * 4);   // [count, gen] + k5cg flip word
       ok &= alloc((void**)&pl->kpart, sizeof(double) * 8 * kMaxRedBlocks);
@@ -471,7 +484,7 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
   }
   {
     const char* fe = std::getenv("NLINV_FRAME");
-    pl->use_frame = (pl->world == 1) && frame_supported(nx) && fe != nullptr && fe[0] == '1';
+    pl->use_frame = !pl->multi && frame_supported(nx) && fe != nullptr && fe[0] == '1';
   }
   if (pl->use_frame) {
     ok &= alloc((void**)&pl->fred, sizeof(double) * 3 * 6 * kMaxFrameBlocks);
@@ -518,10 +531,12 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
     return fail(nullptr, NLINV_ERR_CUDA, msg);
   }
 #ifdef NLINV_WITH_NCCL
-  if (pl->world > 1) {
+  if (pl->multi) {
     ncclUniqueId uid;
-    std::memcpy(&uid, p->nccl_id, 128);
-    ncclResult_t r = ncclCommInitRank(&pl->comm, pl->world, uid, pl->rank);
+    ncclResult_t r = ncclSuccess;
+    if (pl->world > 1) std::memcpy(&uid, p->nccl_id, 128);
+    else r = ncclGetUniqueId(&uid);   // NLINV_FORCE_NCCL=1: one-rank communicator (test mode)
+    if (r == ncclSuccess) r = ncclCommInitRank(&pl->comm, pl->world, uid, pl->rank);
     if (r != ncclSuccess) {
       std::string msg = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
       pl->comm = nullptr;
@@ -637,7 +652,7 @@ struct Enq {
   }
   // all-reduce (sum) over the coil shards; in place when src == dst. No-op for world == 1.
   nlinv_status allreduce_f(const float* src, float* dst, size_t count) {
-    if (pl->world == 1) return NLINV_OK;
+    if (!pl->multi) return NLINV_OK;
 #ifdef NLINV_WITH_NCCL
     NC(ncclAllReduce(src, dst, count, ncclFloat, ncclSum, pl->comm, s));
 #endif
@@ -645,7 +660,7 @@ struct Enq {
   }
   nlinv_status allreduce_scalar(int slot) { return allreduce_scalars(slot, 1); }
   nlinv_status allreduce_scalars(int slot, int count) {
-    if (pl->world == 1) return NLINV_OK;
+    if (!pl->multi) return NLINV_OK;
 #ifdef NLINV_WITH_NCCL
     NC(ncclAllReduce(pl->scal + slot, pl->scal + slot, count, ncclDouble, ncclSum, pl->comm, s));
 #endif
@@ -710,7 +725,7 @@ nlinv_status enq_k4_allreduce(Enq& q) {
   ra.out = pl->tB;
   ra.S = pl->S_all;   // one plane per K4 coil chunk
   TRY(q.row(RK_K4, ra));
-  if (pl->world > 1) {
+  if (pl->multi) {
     const int np = k4_planes(pl->ng, pl->J);
     TRY(q.kern("coil_sum", [&] { return launch_coil_sum(pl->ng, pl->S_all, np, pl->S, q.s); }));
     TRY(q.allreduce_f((const float*)pl->S, (float*)pl->S_sum, 2 * pl->Q));
@@ -720,7 +735,7 @@ nlinv_status enq_k4_allreduce(Enq& q) {
 
 // the coil-sum planes the rho slices add up (chunk planes in order, or the rank-summed plane)
 void set_S(nlinv_plan pl, ColArgs& c) {
-  if (pl->world > 1) {
+  if (pl->multi) {
     c.S = pl->S_sum;
     c.nS = 1;
   } else {
@@ -929,7 +944,7 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
     ra.xrho = x;
     ra.rss = pl->rss_all;
     TRY(q.row(RK_RSS, ra));
-    if (pl->world > 1) {
+    if (pl->multi) {
       TRY(q.kern("rss_sum", [&] { return launch_rss_sum(pl->ng, pl->rss_all, pl->J, pl->rss, q.s); }));
       TRY(q.allreduce_f(pl->rss, pl->rss_sum, pl->Q));
       TRY(q.kern("image", [&] { return launch_image(pl->ng, pl->rho_omega, pl->rss_sum, 1, img, q.s); }));

@@ -308,6 +308,7 @@ VARIANTS = {
     "unfused K1/K5": {"NLINV_FUSE_K1": "0", "NLINV_FUSE_K5": "0"},
     "K5+update only": {"NLINV_FUSE_K1": "0"},
     "rho in own CTAs": {"NLINV_RHO_SPREAD": "0"},
+    "multi-GPU code path, one-rank NCCL communicator": {"NLINV_FORCE_NCCL": "1"},
     "persistent frame kernel": {"NLINV_FRAME": "1", "NLINV_DATAFLOW": "0"},
     "frame kernel, dataflow": {"NLINV_FRAME": "1", "NLINV_DATAFLOW": "1"},
 }
