@@ -241,18 +241,25 @@ template <int L, int R, int NS, int RN, class BUF, class SYNC>
 __device__ __forceinline__ void pass_exchange(float2* v, int t, BUF& buf, SYNC sync) {
   using C = Cfg<L>;
   constexpr int E = C::E, T = C::T;
+  // the first exchange (NS == 1) may use a bank-conflict swizzle of the buffer (buf.first)
 #pragma unroll
   for (int m = 0; m < E / R; ++m) {
     const int j = t + T * m;
     const int base = (j / NS) * NS * R + (j % NS);
 #pragma unroll
-    for (int r = 0; r < R; ++r) buf(base + r * NS) = v[m * R + r];
+    for (int r = 0; r < R; ++r) {
+      if constexpr (NS == 1) buf.first(base + r * NS) = v[m * R + r];
+      else buf(base + r * NS) = v[m * R + r];
+    }
   }
   sync();
 #pragma unroll
   for (int m = 0; m < E / RN; ++m) {
 #pragma unroll
-    for (int r = 0; r < RN; ++r) v[m * RN + r] = buf(t + T * m + r * (L / RN));
+    for (int r = 0; r < RN; ++r) {
+      if constexpr (NS == 1) v[m * RN + r] = buf.first(t + T * m + r * (L / RN));
+      else v[m * RN + r] = buf(t + T * m + r * (L / RN));
+    }
   }
   sync();
 }

@@ -45,6 +45,7 @@ struct ColBuf {
   float2* s;
   int c;
   __device__ __forceinline__ float2& operator()(int i) const { return s[i * CW + c]; }
+  __device__ __forceinline__ float2& first(int i) const { return s[i * CW + c]; }
 };
 // Row exchange buffer with an XOR swizzle: slot i lives at i ^ ((i >> 4) & 7). The first Stockham
 // pass stores at stride R (8 at L = 384), which unswizzled puts the 16 lanes of a transform on two
@@ -53,7 +54,10 @@ struct ColBuf {
 __host__ __device__ constexpr int rsw(int i) { return i ^ ((i >> 4) & 7); }
 struct RowBuf {
   float2* s;
-  __device__ __forceinline__ float2& operator()(int i) const { return s[rsw(i)]; }
+  __device__ __forceinline__ float2& operator()(int i) const { return s[i]; }
+  // first Stockham exchange only (the stride-R stores): the later exchanges are conflict-light
+  // unswizzled, and the swizzle's index arithmetic is not free in these issue-bound passes
+  __device__ __forceinline__ float2& first(int i) const { return s[(i & ~15) | ((i & 15) ^ ((i >> 4) & 7))]; }
 };
 
 __device__ __forceinline__ float sgn_of(int i) { return (i & 1) ? -1.0f : 1.0f; }
@@ -1274,7 +1278,7 @@ __device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, int jlo, i
     __syncthreads();
     for (int xx = tid; xx < n; xx += nt) {
       float2 sacc = accs[xx];
-      for (int gg = 0; gg < GPC && j0 + gg < jhi; ++gg) sacc = cadd(sacc, xbase[(size_t)gg * L + rsw(xx)]);
+      for (int gg = 0; gg < GPC && j0 + gg < jhi; ++gg) sacc = cadd(sacc, xbase[(size_t)gg * L + xx]);
       accs[xx] = sacc;
     }
     __syncthreads();
