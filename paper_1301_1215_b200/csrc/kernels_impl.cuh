@@ -183,6 +183,19 @@ __device__ __forceinline__ float cg_beta(const double* scal, int i) {  // beta_i
   return rr != 0.0 ? (float)(cg_rr(scal, i + 1) / rr) : 0.0f;
 }
 
+// Single-reduction CG scalars of iteration i (R19): gamma_i = <r_i,r_i>/<p_i,Ap_i> with the direct
+// <r_i,r_i>; <r_{i+1},r_{i+1}> by exact expansion (rho and chat parts), beta_i = that / <r_i,r_i>.
+__device__ __forceinline__ void cg1_gamma_beta(const double* scal, int i, float* gamma, float* beta) {
+  const double rrr = scal[SC_RR_RHO + i], rrc = scal[SC_RR_CHAT + i], rr = rrr + rrc;
+  const double pap = scal[SC_PAP_RHO + i] + scal[SC_PAP_CHAT + i];
+  const float g = rr != 0.0 ? (float)(rr / pap) : 0.0f;
+  const double gd = (double)g;
+  const double nr = fmax(rrr - 2.0 * gd * scal[SC_RAP_RHO + i] + gd * gd * scal[SC_AA_RHO + i], 0.0);
+  const double nc = fmax(rrc - 2.0 * gd * scal[SC_RAP_CHAT + i] + gd * gd * scal[SC_AA_CHAT + i], 0.0);
+  *gamma = g;
+  *beta = rr != 0.0 ? (float)((nr + nc) / rr) : 0.0f;
+}
+
 // Programmatic dependent launch (PDL): every pass is launched with programmatic stream
 // serialisation, so its CTAs are scheduled while the previous pass drains; pdl_wait() blocks
 // until the previous grid has completed and its memory is visible, so it must precede every
@@ -262,7 +275,13 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
     if (j == a.J) {  // rho-block slice of the fused CG step (same update as the coil tiles below)
       for (int y = rlo + t; y < rhi; y += T) {
         const size_t i = (size_t)y * L + x;
-        const float2 rv = a.rho_r[i], pv = a.rho_p[i];
+        float2 rv = a.rho_r[i];
+        const float2 pv = a.rho_p[i];
+        if (a.cg1 && a.iter > 0) {   // r_i = r_{i-1} - gamma A p_{i-1}
+          const float2 av = a.rho_a[i];
+          rv = make_float2(fmaf(-a.gamma, av.x, rv.x), fmaf(-a.gamma, av.y, rv.y));
+          a.rho_r[i] = rv;
+        }
         if (a.iter > 0) {
           const float2 dv = (a.iter > 1) ? a.rho_dx[i] : make_float2(0.f, 0.f);
           a.rho_dx[i] = make_float2(fmaf(a.gamma, pv.x, dv.x), fmaf(a.gamma, pv.y, dv.y));
@@ -289,6 +308,12 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
           const float2 o = make_float2(fmaf(a.alpha, pv.x, sv.x), fmaf(a.alpha, pv.y, sv.y));
           a.rho_out[i] = o;
           acc_rho += (double)pv.x * o.x + (double)pv.y * o.y;
+          if (a.cg1) {
+            const float2 rv = a.rho_r[i];
+            acc3[0] += (double)rv.x * o.x + (double)rv.y * o.y;
+            acc3[1] += (double)o.x * o.x + (double)o.y * o.y;
+            acc3[2] += (double)rv.x * rv.x + (double)rv.y * rv.y;
+          }
         } else if constexpr (MODE == CK_FFT_W_RHS) {
           const float2 d = csub(a.rho_a[i], a.rho_b[i]);
           const float2 b = make_float2(fmaf(-a.alpha, d.x, sv.x), fmaf(-a.alpha, d.y, sv.y));
@@ -314,7 +339,13 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
       const size_t lo = (size_t)stripe * chunk, hi = (lo + chunk < N) ? lo + chunk : N;
       for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         if constexpr (MODE == CK_IFFT_W_CG) {
-          const float2 rv = a.rho_r[i], pv = a.rho_p[i];
+          float2 rv = a.rho_r[i];
+          const float2 pv = a.rho_p[i];
+          if (a.cg1 && a.iter > 0) {
+            const float2 av = a.rho_a[i];
+            rv = make_float2(fmaf(-a.gamma, av.x, rv.x), fmaf(-a.gamma, av.y, rv.y));
+            a.rho_r[i] = rv;
+          }
           if (a.iter > 0) {
             const float2 dv = (a.iter > 1) ? a.rho_dx[i] : make_float2(0.f, 0.f);
             a.rho_dx[i] = make_float2(fmaf(a.gamma, pv.x, dv.x), fmaf(a.gamma, pv.y, dv.y));
@@ -332,6 +363,12 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
             const float2 o = make_float2(fmaf(a.alpha, pv.x, sv.x), fmaf(a.alpha, pv.y, sv.y));
             a.rho_out[i] = o;
             acc_rho += (double)pv.x * o.x + (double)pv.y * o.y;
+            if (a.cg1) {
+              const float2 rv = a.rho_r[i];
+              acc3[0] += (double)rv.x * o.x + (double)rv.y * o.y;
+              acc3[1] += (double)o.x * o.x + (double)o.y * o.y;
+              acc3[2] += (double)rv.x * rv.x + (double)rv.y * rv.y;
+            }
           } else if constexpr (MODE == CK_FFT_W_RHS) {
             const float2 d = csub(a.rho_a[i], a.rho_b[i]);
             const float2 b = make_float2(fmaf(-a.alpha, d.x, sv.x), fmaf(-a.alpha, d.y, sv.y));
@@ -380,11 +417,16 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
         rv[u] = a.r[i];
         pv[u] = a.p[i];
         dv[u] = hasdx ? a.dx[i] : make_float2(0.f, 0.f);
+        if (a.cg1 && upd) {   // r_i = r_{i-1} - gamma A p_{i-1} (single-reduction CG, R19)
+          const float2 av = a.src2[i];
+          rv[u] = make_float2(fmaf(-a.gamma, av.x, rv[u].x), fmaf(-a.gamma, av.y, rv[u].y));
+        }
       }
 #pragma unroll
       for (int u = 0; u < CH; ++u) {
         const int yr = S::in_idx(t, e0 + u);
         const size_t i = j * N + (size_t)yr * L + x;
+        if (a.cg1 && upd) a.r[i] = rv[u];
         if (upd) a.dx[i] = make_float2(fmaf(a.gamma, pv[u].x, dv[u].x), fmaf(a.gamma, pv[u].y, dv[u].y));
         const float2 sv = make_float2(fmaf(a.beta, pv[u].x, rv[u].x), fmaf(a.beta, pv[u].y, rv[u].y));
         a.p[i] = sv;
@@ -479,7 +521,10 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
       for (int u = 0; u < CH; ++u) {
         const size_t i = (size_t)S::out_idx(t, e0 + u) * L + x;
         wv[u] = a.winv[i];
-        if constexpr (MODE == CK_FFT_W_NORMAL) o1[u] = a.src2[j * N + i];
+        if constexpr (MODE == CK_FFT_W_NORMAL) {
+          o1[u] = a.src2[j * N + i];
+          if (a.cg1) o2[u] = a.r[j * N + i];
+        }
         if constexpr (MODE == CK_FFT_W_RHS) {
           o1[u] = a.src[j * N + i];
           o2[u] = a.src2[j * N + i];
@@ -496,6 +541,12 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
           if (a.fuse_update) v[e0 + u] = o;   // A p stays in registers for the fused r update
           else a.out[j * N + i] = o;
           acc += (double)pv.x * o.x + (double)pv.y * o.y;
+          if (a.cg1) {
+            const float2 rv = o2[u];
+            acc3[3] += (double)rv.x * o.x + (double)rv.y * o.y;
+            acc3[4] += (double)o.x * o.x + (double)o.y * o.y;
+            acc3[5] += (double)rv.x * rv.x + (double)rv.y * rv.y;
+          }
         } else if constexpr (MODE == CK_FFT_W_RHS) {
           const float2 d = csub(o1[u], o2[u]);
           const float2 b = make_float2(fmaf(-a.alpha, d.x, val.x), fmaf(-a.alpha, d.y, val.y));
@@ -715,14 +766,19 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColAr
   pdl_wait();
   pdl_trigger();
   if constexpr (MODE == CK_IFFT_W_CG) {
-    a.gamma = (a.iter > 0) ? cg_gamma(a.scal, a.iter - 1) : 0.0f;
-    a.beta = (a.iter > 0) ? cg_beta(a.scal, a.iter - 1) : 0.0f;
+    if (a.cg1) {
+      if (a.iter > 0) cg1_gamma_beta(a.scal, a.iter - 1, &a.gamma, &a.beta);
+      else a.gamma = a.beta = 0.0f;
+    } else {
+      a.gamma = (a.iter > 0) ? cg_gamma(a.scal, a.iter - 1) : 0.0f;
+      a.beta = (a.iter > 0) ? cg_beta(a.scal, a.iter - 1) : 0.0f;
+    }
   }
   double acc_rho = 0.0, acc = 0.0;
   // the rho slice (when present) is blockIdx.y == 0 so it is scheduled first
   const bool has_rho = (MODE == CK_IFFT_W_CG || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ);
   const int j = (has_rho && !a.rho_spread) ? (blockIdx.y == 0 ? a.J : (int)blockIdx.y - 1) : (int)blockIdx.y;
-  double acc3[4] = {0.0, 0.0, 0.0, 0.0};
+  double acc3[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};   // single-reduction CG dots (rho: 0-2, chat: 3-5)
   col_task<L, MODE>(a, blockIdx.x, j, tw, xb, acc_rho, acc, acc3, 0, L, true, MODE == CK_PSF ? &mb : nullptr);
   trace_stamp(a.trace, 5);
   if constexpr (MODE == CK_RESADJ || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_NORMAL) {
@@ -732,6 +788,11 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColAr
         const int sl[2] = {SC_RR_RHO + a.iter + 1, SC_RR_CHAT + a.iter + 1};
         grid_finish<2>(vv, a.partials, a.counter, a.scal_w, sl, red);
       }
+    } else if (MODE == CK_FFT_W_NORMAL && a.cg1 && a.partials != nullptr) {
+      const double vv[8] = {acc_rho, acc, acc3[0], acc3[3], acc3[1], acc3[4], acc3[2], acc3[5]};
+      const int sl[8] = {SC_PAP_RHO + a.iter, SC_PAP_CHAT + a.iter, SC_RAP_RHO + a.iter, SC_RAP_CHAT + a.iter,
+                         SC_AA_RHO + a.iter,  SC_AA_CHAT + a.iter,  SC_RR_RHO + a.iter,  SC_RR_CHAT + a.iter};
+      grid_finish<8>(vv, a.partials, a.counter, a.scal_w, sl, red);
     } else if (a.partials != nullptr) {
       const double vv[2] = {acc_rho, acc};
       const int sl[2] = {a.out_slot_rho, a.out_slot};
@@ -1722,7 +1783,7 @@ __global__ void __launch_bounds__(256, 2) frame_kernel(FrameArgs f) {
     { double a3[4]; col_phase<L, CK_FFT_W_RHS>(ca, tw, xb, J + 1, d0, d1, a3); }
     double2 rr2 = grid_reduce2(d0, d1, f.red + 1 * 6 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
     stamp(f, nstamp);
-    double acc3[4];
+    double acc3[6];
     double rr = rr2.x + rr2.y;   // rr_0
     float gamma = 0.0f, beta = 0.0f;
     if (blockIdx.x == 0 && threadIdx.x == 0) {

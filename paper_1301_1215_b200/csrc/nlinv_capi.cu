@@ -72,6 +72,7 @@ struct nlinv_plan_s {
   bool fuse_k5 = false;                   // K5 + r update as one cooperative pass (world == 1, fits one wave)
   bool fuse_k1 = false;                   // ... also K1 of the next iteration / the Newton update
   bool k5cg1 = false;                     // fused K5 + CG + K1 with a single grid barrier (k5cg_kernel)
+  bool cg1 = false;                       // unfused CG: one (grouped) scalar all-reduce per iteration (R19)
   unsigned* kbar = nullptr;               // its grid barrier
   double* kpart = nullptr;                // its <p, Ap> partials
   unsigned long long* trace = nullptr;
@@ -470,6 +471,10 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
   {
     const char* rs = std::getenv("NLINV_RHO_SPREAD");
     pl->rho_spread = !(rs && rs[0] == '0');
+    // single-reduction unfused CG: default where a reduction is a collective (multi-GPU path); on
+    // one GPU the r update is cheaper as its own pass (measured), NLINV_CG1=1 forces it there
+    const char* c1 = std::getenv("NLINV_CG1");
+    pl->cg1 = c1 ? (c1[0] == '1') : pl->multi;
     const char* fk = std::getenv("NLINV_FUSE_K5");
     pl->fuse_k5 = pl->rho_spread && !pl->multi && !(fk && fk[0] == '0') && col_fusable(nx, pl->J);
     if (pl->fuse_k5) {
@@ -495,7 +500,7 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
     pl->dataflow = !(df && df[0] == '0');
   }
   ok &= alloc((void**)&pl->scal, sizeof(double) * SC_TOTAL);
-  ok &= alloc((void**)&pl->partials, sizeof(double) * 6 * kMaxRedBlocks);
+  ok &= alloc((void**)&pl->partials, sizeof(double) * 8 * kMaxRedBlocks);
   ok &= alloc((void**)&pl->counter, sizeof(unsigned) * 4);
   if (!ok) {
     plan_free(pl);
@@ -659,6 +664,17 @@ struct Enq {
     return NLINV_OK;
   }
   nlinv_status allreduce_scalar(int slot) { return allreduce_scalars(slot, 1); }
+  // several single-double all-reduces aggregated into one NCCL launch (ncclGroupStart/End)
+  nlinv_status allreduce_group(const int* slots, int n) {
+    if (!pl->multi) return NLINV_OK;
+#ifdef NLINV_WITH_NCCL
+    NC(ncclGroupStart());
+    for (int k = 0; k < n; ++k)
+      NC(ncclAllReduce(pl->scal + slots[k], pl->scal + slots[k], 1, ncclDouble, ncclSum, pl->comm, s));
+    NC(ncclGroupEnd());
+#endif
+    return NLINV_OK;
+  }
   nlinv_status allreduce_scalars(int slot, int count) {
     if (!pl->multi) return NLINV_OK;
 #ifdef NLINV_WITH_NCCL
@@ -703,6 +719,11 @@ nlinv_status enq_derivative_head(Enq& q, const float2* dx, bool cg_fused, int it
     ca.rho_p = pl->p;
     ca.rho_dx = pl->dx;
     ca.iter = iter;
+    if (pl->cg1 && !pl->fuse_k5) {   // r -= gamma A p of the previous iteration happens here (R19)
+      ca.cg1 = 1;
+      ca.src2 = pl->Ap + pl->N;
+      ca.rho_a = pl->Ap;
+    }
     TRY(q.col(CK_IFFT_W_CG, ca));
   } else {
     ca.src = dx + pl->N;
@@ -764,6 +785,13 @@ nlinv_status enq_normal(Enq& q, float alpha, const float2* dx, float2* out, bool
   cb.partials = cg ? pl->partials : nullptr;
   cb.out_slot = SC_PAP_CHAT + iter;
   cb.out_slot_rho = SC_PAP_RHO + iter;
+  cb.iter = iter;
+  const bool cg1 = cg && pl->cg1 && !pl->fuse_k5;
+  if (cg1) {   // also <r,Ap>, <Ap,Ap>, <r,r> for the single reduction (R19)
+    cb.cg1 = 1;
+    cb.r = pl->r + pl->N;
+    cb.rho_r = pl->r;
+  }
   if (cg && pl->fuse_k5) {
     cb.fuse_update = 1;
     cb.last_iter = (iter == last_iter) ? 1 : 0;
@@ -775,7 +803,12 @@ nlinv_status enq_normal(Enq& q, float alpha, const float2* dx, float2* out, bool
     cb.iter = iter;
   }
   TRY(q.col(CK_FFT_W_NORMAL, cb));
-  if (cg) TRY(q.allreduce_scalar(SC_PAP_CHAT + iter));   // chat part; the rho part is replicated
+  if (cg1) {   // ONE grouped all-reduce of the four chat parts (the rho parts are replicated)
+    const int slots[4] = {SC_PAP_CHAT + iter, SC_RAP_CHAT + iter, SC_AA_CHAT + iter, SC_RR_CHAT + iter};
+    TRY(q.allreduce_group(slots, 4));
+  } else if (cg) {
+    TRY(q.allreduce_scalar(SC_PAP_CHAT + iter));   // chat part; the rho part is replicated
+  }
   return NLINV_OK;
 }
 
@@ -917,7 +950,7 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
     // CG: L iterations of the normal operator + vector updates
     for (int it = 0; it < L; ++it) {
       TRY(enq_normal(q, alpha, pl->p, pl->Ap, true, it, L - 1));
-      if (it < L - 1 && !pl->fuse_k5) {  // r -= gamma Ap, <r, r> (dx is updated inside the next K1)
+      if (it < L - 1 && !pl->fuse_k5 && !pl->cg1) {  // r -= gamma Ap, <r, r> (dx is updated inside the next K1)
         VecArgs vr = q.vec();
         vr.r = pl->r;
         vr.Ap = pl->Ap;

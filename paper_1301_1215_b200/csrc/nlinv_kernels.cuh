@@ -14,7 +14,11 @@ constexpr int SC_RR_CHAT = SC_RR_RHO + kMaxCG + 1;   // <r_i, r_i> chat blocks  
 constexpr int SC_PAP_RHO = SC_RR_CHAT + kMaxCG + 1;  // Re<p_i, A p_i> rho       [kMaxCG]
 constexpr int SC_PAP_CHAT = SC_PAP_RHO + kMaxCG;     // Re<p_i, A p_i> chat      [kMaxCG]
 constexpr int SC_RES = SC_PAP_CHAT + kMaxCG;         // ||P y - F(x_n)||^2       [kMaxNewton]
-constexpr int SC_TOTAL = SC_RES + kMaxNewton;
+constexpr int SC_RAP_RHO = SC_RES + kMaxNewton;      // Re<r_i, A p_i> rho  (single-reduction CG, R19)
+constexpr int SC_RAP_CHAT = SC_RAP_RHO + kMaxCG;     // Re<r_i, A p_i> chat
+constexpr int SC_AA_RHO = SC_RAP_CHAT + kMaxCG;      // <A p_i, A p_i> rho
+constexpr int SC_AA_CHAT = SC_AA_RHO + kMaxCG;       // <A p_i, A p_i> chat
+constexpr int SC_TOTAL = SC_AA_CHAT + kMaxCG;
 
 // Reduction slots (each has its own partial array and arrival counter).
 enum RedSlot { RS_A = 0, RS_B = 1, RS_C = 2, RS_COUNT = 3 };
@@ -83,6 +87,8 @@ struct ColArgs {
   float2* xc;              // unknowns, chat blocks (fused Newton update)
   float2* x_rho;           // unknowns, rho block
   int iter;                // CG iteration (beta for CK_IFFT_W_CG)
+  int cg1;                 // unfused single-reduction CG (R19): K5 also forms <r,Ap>, <Ap,Ap>, <r,r>;
+                           // K1 applies r -= gamma Ap (A p from src2 / rho_a) before the p update
   float alpha;
   int J;
 };
