@@ -74,6 +74,22 @@ __device__ __forceinline__ constexpr bool out_is_omega(int e) {
   return (e % R) * (L / R) >= L / 4 && (e % R) * (L / R) < 3 * L / 4;
 }
 
+// Centred transform without sign flips (R1): for even L with L/2 even,
+//   F_c z [k] ∝ (-1)^k FFT((-1)^i z)[k] = FFT(z[. + L/2])[k + L/2],
+// and a shift by L/2 of a pass-0 input (last-pass output) index is a compile-time permutation of
+// the registers (R0, RL even), so the modulations cost no instructions: load register e from
+// index in_idx(t, psh_in(e)), and read position k = out_idx(t, e) from register psh_out(e).
+template <int L>
+__host__ __device__ constexpr int psh_in(int e) {
+  constexpr int R = Cfg<L>::R0;
+  return (e / R) * R + (e % R + R / 2) % R;
+}
+template <int L>
+__host__ __device__ constexpr int psh_out(int e) {
+  constexpr int R = Sched<L>::RL;
+  return (e / R) * R + (e % R + R / 2) % R;
+}
+
 // ------------------------------------------------------------------ deterministic reductions
 // Block sum in a fixed tree (warp xor-shuffles, then warps in index order). Result valid in
 // thread 0. red must hold 32 doubles.
@@ -1169,22 +1185,25 @@ __device__ __forceinline__ void row_task(const RowArgs& a, int pair0, const floa
   {
     const float2* src = a.in + (active ? j * H + (size_t)yy * L : 0);
 #pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = cneg_if(src[S::in_idx(t, e)], S::in_idx(t, e) & 1);
+    for (int e = 0; e < E; ++e) v[e] = src[S::in_idx(t, psh_in<L>(e))];   // half-shifted input (psh_in)
   }
   if (tw_async) tw_wait();
   fft<L, +1>(v, t, tw, buf, SyncWarp{});
-  // v[e] now holds (-1)^k x (row IFFT), k = S::out_idx(t, e); only Omega columns are kept
+  // the centred row IFFT at k = S::out_idx(t, e) is register psh_out(e); only Omega columns are kept
+  float2 w[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) w[e] = v[psh_out<L>(e)];
 
   if constexpr (MODE == RK_SETPOINT || MODE == RK_SETPOINT_FWD || MODE == RK_RSS) {
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int k = S::out_idx(t, e);
       if (out_is_omega<L>(e)) {
-        const float2 cv = cneg_if(v[e], k & 1);
+        const float2 cv = w[e];
         if (active) a.c_omega[j * Q + (size_t)yy * n + (k - q)] = cv;
         if constexpr (MODE == RK_SETPOINT_FWD) {
           const float2 rv = active ? a.xrho[(size_t)row * L + k] : make_float2(0.f, 0.f);
-          v[e] = cscale(cmul(rv, cv), invL * sgn_of(k));
+          v[e] = cscale(cmul(rv, cv), invL);
         } else if constexpr (MODE == RK_RSS) {
           if (active) a.rss[j * Q + (size_t)yy * n + (k - q)] = cv.x * cv.x + cv.y * cv.y;
         }
@@ -1218,9 +1237,9 @@ __device__ __forceinline__ void row_task(const RowArgs& a, int pair0, const floa
     for (int e = 0; e < E; ++e) {
       if (out_is_omega<L>(e)) {
         const int k = S::out_idx(t, e);
-        const float2 dc = cneg_if(v[e], k & 1);
+        const float2 dc = w[e];
         const float2 z = cadd(cmul(pr[u], cv[u]), cmul(rv[u], dc));
-        v[e] = cscale(z, invL * sgn_of(k));
+        v[e] = cscale(z, invL);
         ++u;
       } else {
         v[e] = make_float2(0.f, 0.f);
@@ -1247,10 +1266,10 @@ __device__ __forceinline__ void row_task(const RowArgs& a, int pair0, const floa
     for (int e = 0; e < E; ++e) {
       if (out_is_omega<L>(e)) {
         const int k = S::out_idx(t, e);
-        const float2 uu = cneg_if(v[e], k & 1);
+        const float2 uu = w[e];
         // per-coil term of sum_j conj(c_j) u_j (Table 1 "sum c_j"); summed in coil order by the consumer
         if (active) a.S[j * Q + (size_t)yy * n + (k - q)] = cmulc(cv[u], uu);
-        v[e] = cscale(cmulc(rv[u], uu), invL * sgn_of(k));
+        v[e] = cscale(cmulc(rv[u], uu), invL);
         ++u;
       } else {
         v[e] = make_float2(0.f, 0.f);
@@ -1260,12 +1279,14 @@ __device__ __forceinline__ void row_task(const RowArgs& a, int pair0, const floa
 
   if constexpr (MODE == RK_SETPOINT_FWD || MODE == RK_K2 || MODE == RK_K4) {
     out_to_in<L>(v, t, buf, SyncWarp{});
-    fft<L, -1>(v, t, tw, buf, SyncWarp{});
+#pragma unroll
+    for (int e = 0; e < E; ++e) w[e] = v[psh_in<L>(e)];   // half-shifted input of the row FFT
+    fft<L, -1>(w, t, tw, buf, SyncWarp{});
     if (active) {
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int k = S::out_idx(t, e);
-        a.out[j * H + (size_t)yy * L + k] = cneg_if(v[e], k & 1);
+        a.out[j * H + (size_t)yy * L + k] = w[psh_out<L>(e)];
       }
     }
   }
@@ -1316,10 +1337,13 @@ __device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, int jlo, i
     {  // unconditional loads (see row_task); an inactive group's result is masked below
       const float2* src = a.in + (size_t)(active ? j : jlo) * H + (size_t)yy * L;
 #pragma unroll
-      for (int e = 0; e < E; ++e) v[e] = cneg_if(src[S::in_idx(t, e)], S::in_idx(t, e) & 1);
+      for (int e = 0; e < E; ++e) v[e] = src[S::in_idx(t, psh_in<L>(e))];   // half-shifted (psh_in)
     }
     if (tw_async && j0 == jlo) tw_wait();
     fft<L, +1>(v, t, tw, buf, SyncWarp{});
+    float2 w[E];   // centred IFFT at k = out_idx(t, e) (psh_out)
+#pragma unroll
+    for (int e = 0; e < E; ++e) w[e] = v[psh_out<L>(e)];
     __syncthreads();  // accs / previous chunk's exchange buffers are free
     {
       int u = 0;
@@ -1327,9 +1351,9 @@ __device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, int jlo, i
       for (int e = 0; e < E; ++e) {
         if (out_is_omega<L>(e)) {
           const int k = S::out_idx(t, e);
-          const float2 uu = cneg_if(v[e], k & 1);
+          const float2 uu = w[e];
           buf(k - q) = cmulc(cv[u], uu);
-          v[e] = cscale(cmulc(rv[u], uu), invL * sgn_of(k));
+          v[e] = cscale(cmulc(rv[u], uu), invL);
           ++u;
         } else {
           v[e] = make_float2(0.f, 0.f);
@@ -1344,12 +1368,14 @@ __device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, int jlo, i
     }
     __syncthreads();
     out_to_in<L>(v, t, buf, SyncWarp{});
-    fft<L, -1>(v, t, tw, buf, SyncWarp{});
+#pragma unroll
+    for (int e = 0; e < E; ++e) w[e] = v[psh_in<L>(e)];
+    fft<L, -1>(w, t, tw, buf, SyncWarp{});
     if (active) {
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int k = S::out_idx(t, e);
-        a.out[j * H + (size_t)yy * L + k] = cneg_if(v[e], k & 1);
+        a.out[j * H + (size_t)yy * L + k] = w[psh_out<L>(e)];
       }
     }
   }
