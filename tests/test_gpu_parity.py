@@ -287,6 +287,24 @@ def test_reconstruct_c2_newton_step_full_size():
     plan.close()
 
 
+def test_reconstruct_c4_newton_step_32_coils():
+    """BASELINE config 4 shape (32 coils, 384^2, 15 spokes, T=5): the K5 grid does not fit one
+    co-resident wave, so this runs the unfused multi-kernel CG; one Newton step x 10 CG vs the
+    oracle, warm-started from a prior (frame 1 of a stream)."""
+    B = _B()
+    ng, J = 384, 32
+    y, mask = _frame(ng, J, 15, 5, f=1)
+    prior = c64(synth.random_complex(7, (J + 1, ng, ng))) * np.complex64(0.01)
+    prior[0] += 1.0
+    plan = B.Plan(ng, J, mask)
+    x, img = plan.reconstruct(dev(y), dev(prior), 1, 10)
+    xo, io, hist = _oracle_recon(y, mask, 1, 10, prior=prior)
+    assert rel(host(x), xo) < 1e-4
+    assert rel(host(img), io) < 1e-4
+    assert np.allclose(plan.stats()["residual"][:1], hist[:1], rtol=1e-5)
+    plan.close()
+
+
 @pytest.mark.slow
 def test_reconstruct_c2_full_frame():
     """BASELINE config 2: the full 7 Newton x 10 CG frame vs the oracle (about a minute of CPU)."""
