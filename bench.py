@@ -144,6 +144,15 @@ def make_frames(rank_first: int, count: int):
 
 def run_ours(args):
     import torch
+    if os.environ.get("NLINV_BENCH_STREAM") == "1":
+        torch.cuda.set_device(_dist()[2])
+        with torch.cuda.stream(torch.cuda.Stream()):
+            return _run_ours(args)
+    return _run_ours(args)
+
+
+def _run_ours(args):
+    import torch
     import torch.distributed as dist
     from paper_1301_1215_b200 import Plan
 

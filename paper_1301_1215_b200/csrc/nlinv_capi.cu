@@ -96,6 +96,8 @@ struct nlinv_plan_s {
   // graph cache
   GraphKey gkey;
   cudaGraphExec_t gexec = nullptr;
+  cudaStream_t gstream = nullptr;          // graph stream for callers on the legacy default stream
+  cudaEvent_t gev_in = nullptr, gev_out = nullptr;
   long long gkernels = 0;
   cudaStream_t last_stream = nullptr;
   int last_K = 0, last_L = 0;
@@ -360,6 +362,9 @@ static void plan_free(nlinv_plan pl) {
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
+  if (pl->gev_in) cudaEventDestroy(pl->gev_in);
+  if (pl->gev_out) cudaEventDestroy(pl->gev_out);
+  if (pl->gstream) cudaStreamDestroy(pl->gstream);
   for (cudaEvent_t e : pl->ev_pool) cudaEventDestroy(e);
 #ifdef NLINV_WITH_NCCL
   if (pl->comm) ncclCommDestroy(pl->comm);
@@ -1076,13 +1081,38 @@ extern "C" nlinv_status nlinv_debug_fft2d(nlinv_plan pl, const nlinv_c32* in, nl
 }
 
 // ------------------------------------------------------------------ reconstruct
+static nlinv_status reconstruct_on(nlinv_plan pl, const nlinv_c32* frame, const nlinv_c32* prior, int newton_steps,
+                                   int cg_iters, nlinv_c32* x_out, nlinv_c32* image_out, cudaStream_t s);
+
 extern "C" nlinv_status nlinv_reconstruct(nlinv_plan pl, const nlinv_c32* frame, const nlinv_c32* prior,
                                           int newton_steps, int cg_iters, nlinv_c32* x_out, nlinv_c32* image_out,
                                           void* stream) {
   if (!pl || !frame || !x_out) return fail(pl, NLINV_ERR_ARG, "NULL argument");
   if (newton_steps < 0 || newton_steps > kMaxNewton) return fail(pl, NLINV_ERR_SIZE, "newton_steps out of range");
   if (cg_iters < 1 || cg_iters > kMaxCG) return fail(pl, NLINV_ERR_SIZE, "cg_iters out of range");
-  cudaStream_t s = (cudaStream_t)stream;
+  cudaStream_t us = (cudaStream_t)stream;
+  // A CUDA graph cannot be captured on the legacy default stream: callers on it (e.g. torch's
+  // default stream) get the frame's graph on a plan-owned stream fenced by events on both sides,
+  // so the call stays stream-ordered with respect to `stream`.
+  const bool graphs = !pl->prof && (std::getenv("NLINV_NO_GRAPH") == nullptr);
+  if (us == nullptr && graphs) {
+    if (!pl->gstream) {
+      CU(cudaStreamCreateWithFlags(&pl->gstream, cudaStreamNonBlocking));
+      CU(cudaEventCreateWithFlags(&pl->gev_in, cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&pl->gev_out, cudaEventDisableTiming));
+    }
+    CU(cudaEventRecord(pl->gev_in, us));
+    CU(cudaStreamWaitEvent(pl->gstream, pl->gev_in, 0));
+    nlinv_status st = reconstruct_on(pl, frame, prior, newton_steps, cg_iters, x_out, image_out, pl->gstream);
+    CU(cudaEventRecord(pl->gev_out, pl->gstream));
+    CU(cudaStreamWaitEvent(us, pl->gev_out, 0));
+    return st;
+  }
+  return reconstruct_on(pl, frame, prior, newton_steps, cg_iters, x_out, image_out, us);
+}
+
+static nlinv_status reconstruct_on(nlinv_plan pl, const nlinv_c32* frame, const nlinv_c32* prior, int newton_steps,
+                                   int cg_iters, nlinv_c32* x_out, nlinv_c32* image_out, cudaStream_t s) {
   pl->last_stream = s;
   pl->last_K = newton_steps;
   pl->last_L = cg_iters;
