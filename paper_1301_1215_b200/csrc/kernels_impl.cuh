@@ -1057,7 +1057,10 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
     return;
   }
 
-  // r_{i+1} = r - gamma Ap; dx += gamma p; p_{i+1} = r_{i+1} + beta p; t = w^-1 p_{i+1} (K1 prologue)
+  // r_{i+1} = r - gamma Ap; dx += gamma p (unless dx_side); p_{i+1} = r_{i+1} + beta p (into p_out);
+  // t = w^-1 p_{i+1} (K1 prologue)
+  const bool dxs = a.dx_side != 0;
+  float2* pout = (a.p_out != nullptr) ? a.p_out : a.p;
   {
     constexpr int CH = 8;
 #pragma unroll
@@ -1068,7 +1071,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
       for (int u = 0; u < CH; ++u) {
         const size_t ii = (size_t)S::out_idx(t, e0 + u) * L + x;
         wv[u] = a.winv[ii];
-        dv[u] = hasdx ? a.dx[j * N + ii] : make_float2(0.f, 0.f);
+        dv[u] = (hasdx && !dxs) ? a.dx[j * N + ii] : make_float2(0.f, 0.f);
       }
 #pragma unroll
       for (int u = 0; u < CH; ++u) {
@@ -1077,18 +1080,20 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
         const float2 rv = pf[k * CW + c], pv = buf(k);
         const float2 rn = make_float2(fmaf(-gamma, v[e0 + u].x, rv.x), fmaf(-gamma, v[e0 + u].y, rv.y));
         a.r[i] = rn;
-        a.dx[i] = make_float2(fmaf(gamma, pv.x, dv[u].x), fmaf(gamma, pv.y, dv[u].y));
+        if (!dxs) a.dx[i] = make_float2(fmaf(gamma, pv.x, dv[u].x), fmaf(gamma, pv.y, dv[u].y));
         const float2 pn = make_float2(fmaf(beta, pv.x, rn.x), fmaf(beta, pv.y, rn.y));
-        a.p[i] = pn;
+        pout[i] = pn;
         v[e0 + u] = cscale(pn, wv[u] * sgn_of(k));
       }
     }
   }
   auto update_rho = [&](size_t i, float2 av, float2 rv, float2 pv) {
-    const float2 dv = hasdx ? a.rho_dx[i] : make_float2(0.f, 0.f);
     const float2 rn = make_float2(fmaf(-gamma, av.x, rv.x), fmaf(-gamma, av.y, rv.y));
     a.rho_r[i] = rn;
-    a.rho_dx[i] = make_float2(fmaf(gamma, pv.x, dv.x), fmaf(gamma, pv.y, dv.y));
+    if (!dxs) {
+      const float2 dv = hasdx ? a.rho_dx[i] : make_float2(0.f, 0.f);
+      a.rho_dx[i] = make_float2(fmaf(gamma, pv.x, dv.x), fmaf(gamma, pv.y, dv.y));
+    }
     a.rho_p[i] = make_float2(fmaf(beta, pv.x, rn.x), fmaf(beta, pv.y, rn.y));
   };
   if (sreg) {

@@ -97,6 +97,12 @@ struct nlinv_plan_s {
   GraphKey gkey;
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t gstream = nullptr;          // graph stream for callers on the legacy default stream
+  // fused CG with the dx update on a side stream (dx_side_kernel overlapped with K2-K4):
+  // ping-pong direction buffers p / p2, fork/join events
+  bool dx_side = false;
+  float2* p2 = nullptr;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t gev_in = nullptr, gev_out = nullptr;
   long long gkernels = 0;
   cudaStream_t last_stream = nullptr;
@@ -365,6 +371,10 @@ static void plan_free(nlinv_plan pl) {
   if (pl->gev_in) cudaEventDestroy(pl->gev_in);
   if (pl->gev_out) cudaEventDestroy(pl->gev_out);
   if (pl->gstream) cudaStreamDestroy(pl->gstream);
+  if (pl->ev_fork) cudaEventDestroy(pl->ev_fork);
+  if (pl->ev_join) cudaEventDestroy(pl->ev_join);
+  if (pl->side) cudaStreamDestroy(pl->side);
+  cudaFree(pl->p2);
   for (cudaEvent_t e : pl->ev_pool) cudaEventDestroy(e);
 #ifdef NLINV_WITH_NCCL
   if (pl->comm) ncclCommDestroy(pl->comm);
@@ -490,6 +500,17 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
       // one grid barrier per CG iteration (k5cg_kernel, R19) unless NLINV_K5CG1=0
       const char* g1 = std::getenv("NLINV_K5CG1");
       pl->k5cg1 = pl->fuse_k1 && !(g1 && g1[0] == '0') && k5cg_fusable(nx, pl->J);
+      // dx += gamma p off the critical path on a side stream (NLINV_DX_SIDE=1). Measured on B200 at
+      // C2 it is slower (223 vs 250 fps): the fused pass does not get shorter without its dx traffic
+      // and the side kernel slows K2-K4, so the update stays inside the fused pass by default.
+      const char* ds = std::getenv("NLINV_DX_SIDE");
+      pl->dx_side = pl->k5cg1 && (ds && ds[0] == '1');
+      if (pl->dx_side) {
+        ok &= alloc((void**)&pl->p2, sizeof(float2) * N * nb);
+        ok &= cudaStreamCreateWithFlags(&pl->side, cudaStreamNonBlocking) == cudaSuccess;
+        ok &= cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming) == cudaSuccess;
+        ok &= cudaEventCreateWithFlags(&pl->ev_join, cudaEventDisableTiming) == cudaSuccess;
+      }
     }
   }
   {
@@ -644,6 +665,31 @@ struct Enq {
     a.c_omega = pl->c_omega;
     a.rho_omega = pl->rho_omega;
     return kern(kRowNames[mode], [&] { return launch_row(pl->ng, mode, a, pl->tw, s); });
+  }
+  // fork a kernel onto the plan's side stream (after everything enqueued so far on s) / join it
+  template <class F>
+  nlinv_status fork_side(const char* name, F&& launch) {
+    if (cudaEventRecord(pl->ev_fork, s) != cudaSuccess || cudaStreamWaitEvent(pl->side, pl->ev_fork, 0) != cudaSuccess)
+      return fail(pl, NLINV_ERR_CUDA, "side-stream fork");
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (pl->prof) {
+      e0 = pl->event();
+      cudaEventRecord(e0, pl->side);
+    }
+    cudaError_t e = launch(pl->side);
+    if (pl->prof) {
+      e1 = pl->event();
+      cudaEventRecord(e1, pl->side);
+      pl->prof_rec.push_back({name, e0, e1});
+    }
+    ++kernels;
+    if (e != cudaSuccess) return fail(pl, NLINV_ERR_CUDA, std::string(name) + ": " + cudaGetErrorString(e));
+    if (cudaEventRecord(pl->ev_join, pl->side) != cudaSuccess) return fail(pl, NLINV_ERR_CUDA, "side-stream record");
+    return NLINV_OK;
+  }
+  nlinv_status join_side() {
+    if (cudaStreamWaitEvent(s, pl->ev_join, 0) != cudaSuccess) return fail(pl, NLINV_ERR_CUDA, "side-stream join");
+    return NLINV_OK;
   }
   VecArgs vec() const {
     VecArgs v{};
@@ -909,11 +955,14 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
     if (pl->fuse_k1) {
       // CG, fused form: per iteration K2, K3, K4 and one cooperative pass that does K5,
       // gamma, r -= gamma Ap, <r,r>, beta and K1 of the next iteration (or the Newton update)
+      float2* P[2] = {pl->p, pl->dx_side ? pl->p2 : pl->p};   // p_it lives in P[it % 2]
       for (int it = 0; it < L; ++it) {
+        float2* pc = P[it % 2];
+        float2* pn = P[(it + 1) % 2];
         RowArgs ra{};
         ra.in = pl->tA;
         ra.out = pl->tB;
-        ra.prho = pl->p;
+        ra.prho = pc;
         TRY(q.row(RK_K2, ra));
         ColArgs c3{};
         c3.in = pl->tB;
@@ -922,10 +971,10 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
         TRY(enq_k4_allreduce(q));
         ColArgs c5{};
         c5.in = pl->tB;
-        c5.src2 = pl->p + N;
+        c5.src2 = pc + N;
         c5.out = pl->Ap + N;
         set_S(pl, c5);
-        c5.rho_a = pl->p;
+        c5.rho_a = pc;
         c5.rho_out = pl->Ap;
         c5.alpha = alpha;
         c5.partials = pl->partials;
@@ -938,8 +987,10 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
         c5.iter = it;
         c5.r = pl->r + N;
         c5.rho_r = pl->r;
-        c5.p = pl->p + N;
-        c5.rho_p = pl->p;
+        c5.p = pc + N;
+        c5.rho_p = pn;
+        c5.p_out = pn + N;
+        c5.dx_side = pl->dx_side ? 1 : 0;
         c5.dx = pl->dx + N;
         c5.rho_dx = pl->dx;
         c5.t1 = pl->tA;
@@ -948,7 +999,15 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
         c5.bar_count = pl->kbar;
         c5.bar_gen = pl->kbar + 1;
         c5.fpart = pl->kpart;
+        if (pl->dx_side && it > 0) TRY(q.join_side());   // dx_side(it - 1) read p_{it-1} = P[(it+1) % 2]
         TRY(q.col(pl->k5cg1 ? CK_K5CG : CK_FFT_W_NORMAL, c5));
+        if (pl->dx_side && it < L - 1) {                  // dx += gamma_it p_it, overlapped with K2-K4
+          VecArgs vd = q.vec();
+          vd.dx = pl->dx;
+          vd.p = pc;
+          vd.iter = it;
+          TRY(q.fork_side("dx_side", [&](cudaStream_t ss) { return launch_dx_side(vd, ss); }));
+        }
       }
       continue;
     }

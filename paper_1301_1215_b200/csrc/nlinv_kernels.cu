@@ -92,6 +92,24 @@ __global__ void __launch_bounds__(kVecThreads) newton_update_kernel(VecArgs a) {
   }
 }
 
+// dx += gamma_i p_i off the critical path (fused CG with dx_side): runs on a side stream, overlapped
+// with K2-K4 of the next iteration; p_i is the previous buffer of the ping-pong pair (the fused pass
+// wrote p_{i+1} into the other one). gamma_i from the same scalars, in the same order, as the pass.
+__global__ void __launch_bounds__(kVecThreads) dx_side_kernel(VecArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  const float gamma = cg_gamma(a.scal, a.iter);
+  const bool hasdx = a.iter > 0;
+  const long long n2 = a.ntot / 2, stride = (long long)gridDim.x * blockDim.x;
+  const float4* p4 = reinterpret_cast<const float4*>(a.p);
+  float4* dx4 = reinterpret_cast<float4*>(a.dx);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += stride) {
+    const float4 pv = p4[i];
+    const float4 d = hasdx ? dx4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    dx4[i] = make_float4(fmaf(gamma, pv.x, d.x), fmaf(gamma, pv.y, d.y), fmaf(gamma, pv.z, d.z), fmaf(gamma, pv.w, d.w));
+  }
+}
+
 // CG residual update r_{i+1} = r_i - gamma_i A p_i and <r_{i+1}, r_{i+1}> (rho, chat parts)
 __global__ void __launch_bounds__(kVecThreads) r_update_kernel(VecArgs a) {
   __shared__ double red[32];
@@ -184,6 +202,9 @@ static int vec_grid(long long n) {
 
 cudaError_t launch_r_update(int /*ng*/, const VecArgs& a, cudaStream_t s) {
   return launch_k(r_update_kernel, dim3(vec_grid(a.ntot / 2)), dim3(kVecThreads), 0, s, a);
+}
+cudaError_t launch_dx_side(const VecArgs& a, cudaStream_t s) {
+  return launch_k(dx_side_kernel, dim3(vec_grid(a.ntot / 2)), dim3(kVecThreads), 0, s, a);
 }
 cudaError_t launch_newton_update(int /*ng*/, const VecArgs& a, cudaStream_t s) {
   return launch_k(newton_update_kernel, dim3(vec_grid(a.ntot / 2)), dim3(kVecThreads), 0, s, a);

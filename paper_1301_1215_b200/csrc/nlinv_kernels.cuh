@@ -87,6 +87,8 @@ struct ColArgs {
   float2* xc;              // unknowns, chat blocks (fused Newton update)
   float2* x_rho;           // unknowns, rho block
   int iter;                // CG iteration (beta for CK_IFFT_W_CG)
+  float2* p_out;           // fused K5+CG+K1: p_{i+1} destination (ping-pong with p; nullptr = in place)
+  int dx_side;             // fused K5+CG+K1: dx += gamma p is left to dx_side_kernel on a side stream
   int cg1;                 // unfused single-reduction CG (R19): K5 also forms <r,Ap>, <Ap,Ap>, <r,r>;
                            // K1 applies r -= gamma Ap (A p from src2 / rho_a) before the p update
   float alpha;
@@ -173,6 +175,7 @@ cudaError_t launch_frame(int ng, const FrameArgs& f, cudaStream_t s);
 bool frame_supported(int ng);
 cudaError_t launch_mask_compact(const uint8_t* mask, int N, int* counts, int* idx, int* nnz, cudaStream_t s);
 int mask_count_blocks(int N);
+cudaError_t launch_dx_side(const VecArgs& a, cudaStream_t s);
 cudaError_t launch_grid_radial(const float2* raw, int J, int nraw, const int* cells, const int* start, const int* sid,
                                int nnz, size_t N, float2* y, cudaStream_t s);
 cudaError_t launch_scatter_samples(const float2* samples, const int* idx, const int* nnz, int nnz_cap, int J,

@@ -322,6 +322,7 @@ def test_reconstruct_c2_full_frame():
 
 VARIANTS = {
     "fused (default, one grid barrier per CG iteration)": {},
+    "fused, dx update on a side stream (ping-pong p)": {"NLINV_DX_SIDE": "1"},
     "fused, two grid barriers": {"NLINV_K5CG1": "0"},
     "unfused K1/K5, textbook two reductions": {"NLINV_FUSE_K1": "0", "NLINV_FUSE_K5": "0"},
     "unfused K1/K5, single reduction": {"NLINV_FUSE_K1": "0", "NLINV_FUSE_K5": "0", "NLINV_CG1": "1"},
