@@ -26,7 +26,11 @@ template <int L>
 struct ColGeo {
   static constexpr int T = Cfg<L>::T;
   static constexpr int c0 = (256 / T) < 32 ? (256 / T) : 32;
+#ifdef NLV_COLW   // experiment: force the column-tile width
+  static constexpr int CW = (NLV_COLW < c0) ? NLV_COLW : c0;
+#else
   static constexpr int CW = (L % c0 == 0) ? c0 : ((L % 16 == 0 && c0 >= 16) ? 16 : 8);
+#endif
   static constexpr int THREADS = CW * T;
   static constexpr size_t SMEM = sizeof(float2) * (size_t)L * (CW + 1) + 64 * sizeof(double);
   static constexpr size_t SMEM_PF = SMEM + 64 * sizeof(double) + sizeof(float2) * (size_t)L * CW;   // k5cg_kernel
