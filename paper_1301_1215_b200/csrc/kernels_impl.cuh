@@ -1006,6 +1006,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
     __syncthreads();
   }
   // <r_i, r_i>: computed in this pass; the last iteration (no r read) takes the previous pass's value
+  trace_stamp(a.trace, 5);   // post-barrier totals done
   const double rr_r = last ? a.scal[SC_RR_RHO + a.iter] : red[6];
   const double rr_c = last ? a.scal[SC_RR_CHAT + a.iter] : red[7];
   const double rr = rr_r + rr_c;
@@ -1091,6 +1092,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
       }
     }
   }
+  trace_stamp(a.trace, 6);   // coil-tile updates issued
   auto update_rho = [&](size_t i, float2 av, float2 rv, float2 pv) {
     const float2 rn = make_float2(fmaf(-gamma, av.x, rv.x), fmaf(-gamma, av.y, rv.y));
     a.rho_r[i] = rn;
@@ -1133,8 +1135,6 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) k5cg_kernel(ColA
   trace_stamp(a.trace, 0);
   tw_copy_async(tw, twg, L);
   k5cg_task<L>(a, tw, xb, pf, red);   // griddepcontrol.wait inside, after the r prefetch
-  trace_stamp(a.trace, 5);
-  trace_stamp(a.trace, 6);
 }
 
 // ------------------------------------------------------------------ row task (one (coil, Omega row) per group)

@@ -20,10 +20,10 @@ rows = tr[(tr[:, 0] > 0)]
 t0 = rows[:, 0].min()
 rel = (rows - t0) / 1e3
 names = ["start", "tw+loads issued", "fft1 done", "mid done", "fft2 done", "epilogue done", "reduce done"]
-if mode == 9:  # k5cg_kernel (one barrier): 7 = epilogue + dots done, 3 = barrier passed, 4 = updates done
-    order = [0, 1, 2, 7, 3, 4, 5, 6]
+if mode == 9:  # k5cg_kernel (one barrier): 7 = epilogue + dots, 3 = barrier, 5 = totals, 6 = tile updates, 4 = rho updates
+    order = [0, 1, 2, 7, 3, 5, 6, 4]
     names6 = ["start", "prologue + rho stripe", "K5 fft done", "Ap + dots done", "barrier passed",
-              "r/dx/p update done", "K1 fft + T1 store", "end"]
+              "partial totals read", "tile r/dx/p updates issued", "rho stripe updates"]
 if mode == 6:  # fused K5 + CG + K1 (iteration 1): 7 = epilogue done, 3 = barrier 1 passed, 4 = barrier 2 passed
     order = [0, 1, 2, 7, 3, 4, 5, 6]
     names6 = ["start", "prologue loads issued", "K5 fft done", "Ap + <p,Ap> done", "barrier 1 passed",
