@@ -359,3 +359,39 @@ def test_execution_variants_match_oracle(variant, ng, J, spokes, turns, K, L):
     assert rel(host(x), xo) < 1e-4
     assert np.allclose(plan.stats()["residual"], hist, rtol=1e-4)
     plan.close()
+
+
+# 1D FFT sweeps per pass (each pass transforms its rows or columns once or twice)
+_SWEEPS = {"col_ifft_w": 1, "row_setpoint": 1, "row_setpoint_fwd": 2, "col_fwdp": 1, "col_resadj": 2,
+           "col_adj1": 1, "row_k2": 2, "col_psf": 2, "row_k4": 2, "col_fft_w_normal": 1, "col_fft_w_adj": 1,
+           "row_rss": 1}
+
+
+def test_table1_fft_counts_of_the_cuda_passes():
+    """PAPER Table 1 (tests/golden/table1_opcounts.json) on the GPU side: the passes each
+    operator launches carry exactly F: 2, DF: 2, DF^H: 2 two-dimensional transforms (two 1D sweeps
+    each), and DF^H exactly one channel summation (the K4 pass)."""
+    import json
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "table1_opcounts.json")))
+    B = _B()
+    ng, J = 64, 5
+    x, dx, dy = _operands(ng, J, 21)
+    plan = B.Plan(ng, J, O.radial_mask(ng, 11, 1, 0))
+    xd, dxd, dyd = dev(x), dev(dx), dev(dy)
+    y = torch.empty(plan.y_shape, dtype=torch.complex64, device="cuda")
+    out = torch.empty(plan.x_shape, dtype=torch.complex64, device="cuda")
+    plan.set_point(xd)
+    torch.cuda.synchronize()
+    for name, fn in (("F", lambda: plan.forward(xd, y)), ("DF", lambda: plan.derivative(dxd, y)),
+                     ("DFH", lambda: plan.adjoint(dyd, out))):
+        plan.set_profiling(True)
+        fn()
+        prof = plan.profile()
+        plan.set_profiling(False)
+        unknown = [k for k in prof if k not in _SWEEPS]
+        assert not unknown, unknown
+        sweeps = sum(_SWEEPS[k] * v["launches"] for k, v in prof.items())
+        assert sweeps == 2 * gold[name]["fft"], (name, prof)
+        chan_sums = prof.get("row_k4", {"launches": 0})["launches"]
+        assert chan_sums == gold[name]["chan_sum"], (name, prof)
+    plan.close()
