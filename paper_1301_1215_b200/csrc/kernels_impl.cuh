@@ -51,17 +51,17 @@ struct ColBuf {
   __device__ __forceinline__ float2& operator()(int i) const { return s[i * CW + c]; }
   __device__ __forceinline__ float2& first(int i) const { return s[i * CW + c]; }
 };
-// Row exchange buffer with an XOR swizzle: slot i lives at i ^ ((i >> 4) & 7). The first Stockham
-// pass stores at stride R (8 at L = 384), which unswizzled puts the 16 lanes of a transform on two
-// bank pairs (16-way conflict); the swizzle only permutes within aligned 16-slot blocks, so the
-// reads "t + 16 m + const" stay conflict-free and cost one XOR with a compile-time key.
-__host__ __device__ constexpr int rsw(int i) { return i ^ ((i >> 4) & 7); }
+// Row exchange buffer. The first Stockham exchange (buf.first) is XOR-swizzled: slot i lives at
+// (i & ~15) | ((i & 15) ^ ((i >> 4) & 15)). The first pass stores at stride R (8 at L = 384, 16 at
+// L = 1024), which unswizzled puts a warp's lanes on one or two bank pairs; the swizzle permutes
+// within aligned 16-slot blocks, so the reads "t + T m + const" stay conflict-light and cost one
+// XOR with a compile-time key. Later exchanges are unswizzled (conflict-light already).
 struct RowBuf {
   float2* s;
   __device__ __forceinline__ float2& operator()(int i) const { return s[i]; }
   // first Stockham exchange only (the stride-R stores): the later exchanges are conflict-light
   // unswizzled, and the swizzle's index arithmetic is not free in these issue-bound passes
-  __device__ __forceinline__ float2& first(int i) const { return s[(i & ~15) | ((i & 15) ^ ((i >> 4) & 7))]; }
+  __device__ __forceinline__ float2& first(int i) const { return s[(i & ~15) | ((i & 15) ^ ((i >> 4) & 15))]; }
 };
 
 __device__ __forceinline__ float sgn_of(int i) { return (i & 1) ? -1.0f : 1.0f; }
