@@ -89,3 +89,24 @@ def test_nccl_unique_id():
         pytest.skip("built without NCCL")
     a, b = B.get_unique_id(), B.get_unique_id()
     assert len(a) == 128 and a != b
+
+
+def test_pca_and_gridding_entries_validate_before_device():
+    """The f2/f3 entry points reject bad arguments synchronously, before any allocation or launch."""
+    B = _lib()
+    L = B._lib
+    h = ctypes.c_void_p()
+    assert L.nlinv_pca_create(0, 1, ctypes.byref(h)) == 2          # J < 1
+    assert L.nlinv_pca_create(33, 4, ctypes.byref(h)) == 2         # J > 32
+    assert L.nlinv_pca_create(8, 9, ctypes.byref(h)) == 1          # J' > J
+    assert L.nlinv_pca_create(8, 0, ctypes.byref(h)) == 1          # J' < 1
+    assert L.nlinv_pca_create(8, 4, None) == 1
+    assert L.nlinv_pca_fit(None, None, 1, None) == 1
+    assert L.nlinv_pca_apply(None, None, 1, None, None) == 1
+    assert L.nlinv_pca_result(None, None, None, None, None) == 1
+    assert L.nlinv_pca_set_matrix(None, None) == 1
+    assert L.nlinv_pca_destroy(None) == 0
+    assert L.nlinv_pca_launch_count(None) == 0
+    assert L.nlinv_plan_set_trajectory(None, 15, 5) == 1
+    assert L.nlinv_grid_radial(None, 0, None, None, None) == 1
+    assert L.nlinv_stream_frame_radial(None, None, 0, 7, 10, None, None) == 1
