@@ -767,7 +767,7 @@ template <int L, int MODE>
 #define NLV_MINB 2  // <= 128 registers: two 256-thread CTAs per SM (more registers halve residency)
 #endif
 __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColArgs a, const float2* __restrict__ twg) {
-  constexpr int CW = ColGeo<L>::CW, NT = ColGeo<L>::THREADS;
+  constexpr int CW = ColGeo<L>::CW;
   extern __shared__ float4 smem_raw[];
   float2* tw = reinterpret_cast<float2*>(smem_raw);
   float2* xb = tw + L;
@@ -842,7 +842,7 @@ template <int L>
 __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, float2* xb, float2* pf, double* red) {
   using C = Cfg<L>;
   using S = Sched<L>;
-  constexpr int T = C::T, E = C::E, CW = ColGeo<L>::CW;
+  constexpr int E = C::E, CW = ColGeo<L>::CW;
   constexpr int n = L / 2, q = L / 4;
   constexpr size_t N = (size_t)L * L, H = (size_t)n * L, Qs = (size_t)n * n;
   constexpr float invL = 1.0f / (float)L;
@@ -1314,7 +1314,7 @@ __device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, int jlo, i
   constexpr float invL = 1.0f / (float)L;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int g = tid / T, t = tid % T, GPC = nt / T;
-  const int row = q + yy;
+
   RowBuf buf{xbase + (size_t)g * L};
   for (int i = tid; i < n; i += nt) accs[i] = make_float2(0.f, 0.f);
   // rho|Omega of this row is shared by every coil
@@ -1738,7 +1738,7 @@ __device__ __forceinline__ void stamp(const FrameArgs& f, int& ns) {
 
 template <int L>
 __global__ void __launch_bounds__(256, 2) frame_kernel(FrameArgs f) {
-  constexpr int n = L / 2, q = L / 4;
+  constexpr int n = L / 2;
   constexpr size_t N = (size_t)L * L, Q = (size_t)n * n;
   extern __shared__ float4 smem_raw[];
   float2* tw = reinterpret_cast<float2*>(smem_raw);
@@ -2173,7 +2173,7 @@ template <int L, int DIR>
 __global__ void __launch_bounds__(ColGeo<L>::THREADS) fft_cols_tw_kernel(float2* data, const float2* __restrict__ twg) {
   using C = Cfg<L>;
   using S = Sched<L>;
-  constexpr int T = C::T, E = C::E, CW = ColGeo<L>::CW;
+  constexpr int E = C::E, CW = ColGeo<L>::CW;
   constexpr size_t N = (size_t)L * L;
   extern __shared__ float4 smem_raw[];
   float2* tw = reinterpret_cast<float2*>(smem_raw);
