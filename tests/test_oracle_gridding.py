@@ -83,3 +83,55 @@ def test_acquire_radial_is_eq1_termwise():
                 for xx in range(ng):
                     v += img[yy, xx] * np.exp(-2j * np.pi * (kx * (xx - c) + ky * (yy - c)) / ng)
             assert abs(raw[0, s, i] - v / ng) < 1e-12
+
+
+def test_kb_window_closed_forms():
+    # h(0) = 1, symmetric, 0 outside W/2; I0 series against scipy's I0 (an independent routine)
+    import scipy.special as sp
+    W = 4.0
+    b = G.kb_beta(W)
+    assert abs(b - np.pi * np.sqrt((W / 2) ** 2 * 1.5 ** 2 - 0.8)) < 1e-15
+    for z in (0.0, 0.5, 3.0, 8.99, 15.0):
+        assert abs(G._i0(z) - sp.i0(z)) < 1e-12 * sp.i0(z)
+    assert G.kb_window(0.0, W, b) == 1.0
+    for d in (0.3, 1.1, 1.99):
+        assert abs(G.kb_window(d, W, b) - G.kb_window(-d, W, b)) < 1e-15
+        assert abs(G.kb_window(d, W, b) - sp.i0(b * np.sqrt(1 - (2 * d / W) ** 2)) / sp.i0(b)) < 1e-12
+    assert G.kb_window(2.0001, W, b) == 0.0
+
+
+def test_grid_kb_constant_samples_and_psf_footprint():
+    # constant samples -> weighted mean equals the constant wherever the PSF is positive
+    ng, S, T = 24, 3, 1
+    raw = np.full((2, S, ng), 0.75 + 0.5j)
+    y, psf = G.grid_kb(raw, ng, S, T, 0, width=4.0)
+    on = psf > 0
+    assert np.allclose(y[:, on], 0.75 + 0.5j, atol=1e-13) and np.all(y[:, ~on] == 0)
+    # the theta = 0 spoke's centre sample sits exactly on cell (c, c): with S = 1 the PSF there is
+    # the kernel at 0 times itself (1) plus the neighbours' tails along the row
+    y1, psf1 = G.grid_kb(np.ones((1, 1, ng)), ng, 1, 1, 0, width=4.0)
+    c = ng // 2
+    b = G.kb_beta(4.0)
+    h1, h2 = G.kb_window(1.0, 4.0, b), G.kb_window(2.0, 4.0, b)   # h(W/2) = 1 / I0(beta), not 0
+    row = 1.0 + 2 * h1 + 2 * h2                                       # samples at x = c-2 .. c+2
+    assert abs(psf1[c, c] - row) < 1e-13
+    assert abs(psf1[c + 1, c] - h1 * row) < 1e-13                     # one row up: h(1) in y
+    assert abs(psf1[c + 3, c]) == 0.0                                 # beyond W/2
+
+
+def test_grid_kb_is_weighted_least_squares_fit():
+    # y_g(k) minimises sum_s h(k - k_s) |y - d_s|^2 : check the normal equation at a few cells
+    rng = np.random.default_rng(4)
+    ng, S, T = 16, 4, 1
+    raw = rng.standard_normal((1, S, ng)) + 1j * rng.standard_normal((1, S, ng))
+    y, psf = G.grid_kb(raw, ng, S, T, 0, width=3.0)
+    b = G.kb_beta(3.0)
+    traj = synth.radial_trajectory(ng, S, T, 0)
+    c = ng // 2
+    for (gy, gx) in ((c, c), (c + 2, c - 1), (c - 3, c + 3)):
+        w = np.array([[G.kb_window(gx - (c + traj[s, i, 0]), 3.0, b) * G.kb_window(gy - (c + traj[s, i, 1]), 3.0, b)
+                       for i in range(ng)] for s in range(S)])
+        if w.sum() == 0:
+            continue
+        assert abs(w.sum() - psf[gy, gx]) < 1e-12
+        assert abs(np.sum(w * (y[0, gy, gx] - raw[0])) ) < 1e-12 * w.sum() * np.abs(raw).max()
