@@ -232,6 +232,13 @@ long long nlinv_plan_launch_count(nlinv_plan plan);
  * them. Synchronises the device. ERR_STATE if a sample is within 1e-6 of a snap midpoint. */
 nlinv_status nlinv_plan_set_trajectory(nlinv_plan plan, int spokes, int turns);
 
+/* Convolution gridding instead (reading R22): separable Kaiser-Bessel window of `width` grid cells
+ * (0 < width <= 8; beta <= 0 selects Beatty's value for oversampling 2). A sampled cell gets the
+ * window-weighted mean of the samples within width/2 and the frame's P_k becomes real-valued,
+ * P_k = sqrt(PSF), PSF = sum of the window weights (the operators then use P_k on the data and
+ * P_k^2 in the normal operator). Host tables in fp64, weights stored in fp32. Synchronises. */
+nlinv_status nlinv_plan_set_trajectory_kb(nlinv_plan plan, int spokes, int turns, double width, double beta);
+
 /* Grid frame `frame` (phase frame mod turns): writes y[j][cell] for every sampled cell of P_k
  * (other cells untouched: only P_k y enters the method, R16) and sets the plan's P_k to that
  * frame's mask. raw: device [count][spokes][ng]; y: device [count][ng][ng]. Stream-ordered.

@@ -276,7 +276,7 @@ __device__ __forceinline__ void trace_stamp(unsigned long long* tr, int k) {
 // Returns this thread's contributions to the (rho, chat) reductions of MODE. The caller owns
 // the twiddle table tw (shared) and the exchange buffer xb (shared, L*CW float2). Every thread
 // of the CTA must call it (the transform uses __syncthreads).
-template <int L, int MODE>
+template <int L, int MODE, bool PW = false>   // PW: real-valued P_k (KB gridding, R22), a separate instantiation
 __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, const float2* tw, float2* xb,
                                          double& acc_rho, double& acc, double* acc3, int rlo = 0, int rhi = L,
                                          bool tw_async = false, const uint32_t* pre_mbits = nullptr) {
@@ -459,7 +459,8 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
       const int yr = S::in_idx(t, e);
       const size_t i = (size_t)yr * L + x;
       const float2 s = a.in[j * N + i];
-      v[e] = a.mask[i] ? cneg_if(s, yr & 1) : make_float2(0.f, 0.f);
+      if constexpr (PW) v[e] = cscale(cneg_if(s, yr & 1), a.pw[i]);   // real-valued P_k (R22)
+      else v[e] = a.mask[i] ? cneg_if(s, yr & 1) : make_float2(0.f, 0.f);
     }
   } else {  // half-image input: only Omega rows are non-zero
 #pragma unroll
@@ -495,7 +496,22 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
     for (int e = 0; e < E; ++e) {
       const int k = S::out_idx(t, e);
       const bool m = (mbits >> e) & 1u;
-      if constexpr (MODE == CK_PSF) {
+      if constexpr (PW) {   // real-valued P_k = sqrt(PSF) (R22): P_k^2 in the PSF pass
+        const float w = m ? a.pw[(size_t)k * L + x] : 0.f;
+        if constexpr (MODE == CK_PSF) {
+          v[e] = cscale(v[e], w * w);
+        } else {
+          // r = P (y - F_c x): the IFFT consumes (-1)^k P r = P^2 ((-1)^k y - G), ||r||^2 = sum P^2 |.|^2
+          float2 d = make_float2(0.f, 0.f);
+          if (m) {
+            d = csub(cneg_if(a.y[j * N + (size_t)k * L + x], k & 1), v[e]);
+            const float w2 = w * w;
+            acc += (double)w2 * ((double)d.x * d.x + (double)d.y * d.y);
+            d = cscale(d, w2);
+          }
+          v[e] = d;
+        }
+      } else if constexpr (MODE == CK_PSF) {
         // (-1)^k post-sign of the FFT and pre-sign of the IFFT cancel
         v[e] = m ? v[e] : make_float2(0.f, 0.f);
       } else {
@@ -529,7 +545,11 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int k = S::out_idx(t, e);
-      a.out[j * N + (size_t)k * L + x] = ((mbits >> e) & 1u) ? cneg_if(v[e], k & 1) : make_float2(0.f, 0.f);
+      const bool m = (mbits >> e) & 1u;
+      if constexpr (PW)
+        a.out[j * N + (size_t)k * L + x] = m ? cscale(cneg_if(v[e], k & 1), a.pw[(size_t)k * L + x]) : make_float2(0.f, 0.f);
+      else
+        a.out[j * N + (size_t)k * L + x] = m ? cneg_if(v[e], k & 1) : make_float2(0.f, 0.f);
     }
   } else {  // CK_FFT_W_*: operands loaded in chunks so each chunk's loads are in flight together
     constexpr int CH = 8;
@@ -762,7 +782,7 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
   }
 }
 
-template <int L, int MODE>
+template <int L, int MODE, bool PW = false>   // PW: real-valued P_k (KB gridding, R22) -- its own kernel
 #ifndef NLV_MINB
 #define NLV_MINB 2  // <= 128 registers: two 256-thread CTAs per SM (more registers halve residency)
 #endif
@@ -799,7 +819,7 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColAr
   const bool has_rho = (MODE == CK_IFFT_W_CG || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ);
   const int j = (has_rho && !a.rho_spread) ? (blockIdx.y == 0 ? a.J : (int)blockIdx.y - 1) : (int)blockIdx.y;
   double acc3[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};   // single-reduction CG dots (rho: 0-2, chat: 3-5)
-  col_task<L, MODE>(a, blockIdx.x, j, tw, xb, acc_rho, acc, acc3, 0, L, true, MODE == CK_PSF ? &mb : nullptr);
+  col_task<L, MODE, PW>(a, blockIdx.x, j, tw, xb, acc_rho, acc, acc3, 0, L, true, MODE == CK_PSF ? &mb : nullptr);
   trace_stamp(a.trace, 5);
   if constexpr (MODE == CK_RESADJ || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_NORMAL) {
     if (MODE == CK_FFT_W_NORMAL && a.fuse_update) {
@@ -2072,7 +2092,8 @@ static cudaError_t launch_k5cg_t(const ColArgs& a, const float2* tw, cudaStream_
 
 template <int L, int MODE>
 static cudaError_t launch_col_t(const ColArgs& a, const float2* tw, cudaStream_t s) {
-  auto kern = col_kernel<L, MODE>;
+  constexpr bool kPWable = (MODE == CK_PSF || MODE == CK_RESADJ || MODE == CK_FWDP || MODE == CK_ADJ1);
+  auto kern = (kPWable && a.pw != nullptr) ? col_kernel<L, MODE, kPWable> : col_kernel<L, MODE, false>;
   const size_t smem = ColGeo<L>::SMEM;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

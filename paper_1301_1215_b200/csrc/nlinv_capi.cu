@@ -32,11 +32,12 @@ struct GraphKey {
   const void* prior = nullptr;
   const void* xout = nullptr;
   const void* img = nullptr;
+  const void* pw = nullptr;   // real-valued P_k buffer in use (KB gridding) or nullptr
   int K = -1, L = -1;
   cudaStream_t stream = nullptr;
   bool operator==(const GraphKey& o) const {
-    return frame == o.frame && prior == o.prior && xout == o.xout && img == o.img && K == o.K && L == o.L &&
-           stream == o.stream;
+    return frame == o.frame && prior == o.prior && xout == o.xout && img == o.img && pw == o.pw && K == o.K &&
+           L == o.L && stream == o.stream;
   }
 };
 
@@ -90,6 +91,9 @@ struct nlinv_plan_s {
   std::vector<int*> tr_cells, tr_start, tr_sid;
   std::vector<uint8_t*> tr_mask;
   std::vector<int> tr_nnz;
+  std::vector<float*> tr_wgt, tr_pw;   // KB gridding (R22): per-entry weights, sqrt(PSF) per cell
+  const float* pw_active = nullptr;    // real-valued P_k of the current frame (nullptr = binary P_k)
+  float* pw_buf = nullptr;             // fixed device copy of the frame's sqrt(PSF) (graph-stable pointer)
   float2* h_raw = nullptr;   // staging of host raw samples (nlinv_stream_frame_radial)
   void* slab = nullptr;      // one allocation for the per-iteration working set (L2 access window)
   long long mnnz_host = -1;  // count of midx; -1 = index list stale (P_k changed)
@@ -252,6 +256,11 @@ static nlinv_status traj_clear(nlinv_plan pl) {
   for (int* p : pl->tr_start) cudaFree(p);
   for (int* p : pl->tr_sid) cudaFree(p);
   for (uint8_t* p : pl->tr_mask) cudaFree(p);
+  for (float* p : pl->tr_wgt) cudaFree(p);
+  for (float* p : pl->tr_pw) cudaFree(p);
+  pl->tr_wgt.clear();
+  pl->tr_pw.clear();
+  pl->pw_active = nullptr;
   pl->tr_cells.clear();
   pl->tr_start.clear();
   pl->tr_sid.clear();
@@ -323,6 +332,100 @@ extern "C" nlinv_status nlinv_plan_set_trajectory(nlinv_plan pl, int spokes, int
   return NLINV_OK;
 }
 
+// Kaiser-Bessel window (R22): I0 by its power series, Beatty's beta for oversampling 2 when beta <= 0
+static double kb_i0(double z) {
+  double term = 1.0, s = 1.0;
+  const double q = 0.25 * z * z;
+  for (int k = 1; term > 1e-17 * s; ++k) {
+    term *= q / ((double)k * (double)k);
+    s += term;
+  }
+  return s;
+}
+static double kb_h(double d, double width, double beta, double i0b) {
+  const double u = 2.0 * d / width;
+  if (std::fabs(u) > 1.0) return 0.0;
+  return kb_i0(beta * std::sqrt(1.0 - u * u)) / i0b;
+}
+
+extern "C" nlinv_status nlinv_plan_set_trajectory_kb(nlinv_plan pl, int spokes, int turns, double width, double beta) {
+  if (!pl) return fail(pl, NLINV_ERR_ARG, "NULL plan");
+  if (spokes < 1 || turns < 1 || turns > 64) return fail(pl, NLINV_ERR_ARG, "bad spokes/turns");
+  if (!(width > 0.0 && width <= 8.0)) return fail(pl, NLINV_ERR_ARG, "KB width must be in (0, 8] cells");
+  if (beta <= 0.0) beta = M_PI * std::sqrt((width / 2.0) * (width / 2.0) * 2.25 - 0.8);
+  CU(cudaDeviceSynchronize());
+  traj_clear(pl);
+  const int ng = pl->ng;
+  const size_t N = pl->N;
+  const double denom = (double)spokes * (double)turns, half = width / 2.0, c = (double)(ng / 2);
+  const double i0b = kb_i0(beta);
+  for (int f = 0; f < turns; ++f) {
+    struct Ent { int cell, sid; double h; };
+    std::vector<Ent> es;
+    for (int sp = 0; sp < spokes; ++sp) {
+      const double theta = M_PI * (double)(sp * turns + f) / denom;
+      const double ct = std::cos(theta), st = std::sin(theta);
+      for (int i = 0; i < ng; ++i) {
+        const double rr = (double)(i - ng / 2);
+        const double kx = c + rr * ct, ky = c + rr * st;
+        for (long long gy = (long long)std::ceil(ky - half); gy <= (long long)std::floor(ky + half); ++gy) {
+          const double hy = kb_h((double)gy - ky, width, beta, i0b);
+          if (hy == 0.0 || gy < 0 || gy >= ng) continue;
+          for (long long gx = (long long)std::ceil(kx - half); gx <= (long long)std::floor(kx + half); ++gx) {
+            const double hx = kb_h((double)gx - kx, width, beta, i0b);
+            if (hx == 0.0 || gx < 0 || gx >= ng) continue;
+            es.push_back({(int)(gy * ng + gx), sp * ng + i, hx * hy});
+          }
+        }
+      }
+    }
+    std::stable_sort(es.begin(), es.end(), [](const Ent& a, const Ent& b) { return a.cell < b.cell; });
+    std::vector<int> cells, start, sid;
+    std::vector<float> wgt, pw(N, 0.0f);
+    std::vector<uint8_t> m(N, 0);
+    double psf = 0.0;
+    for (size_t u = 0; u < es.size(); ++u) {
+      if (u == 0 || es[u].cell != es[u - 1].cell) {
+        if (u > 0) pw[es[u - 1].cell] = (float)std::sqrt(psf);
+        cells.push_back(es[u].cell);
+        start.push_back((int)u);
+        m[es[u].cell] = 1;
+        psf = 0.0;
+      }
+      psf += es[u].h;
+      sid.push_back(es[u].sid);
+      wgt.push_back((float)es[u].h);
+    }
+    if (!es.empty()) pw[es.back().cell] = (float)std::sqrt(psf);
+    start.push_back((int)es.size());
+    int *dc = nullptr, *ds = nullptr, *di = nullptr;
+    uint8_t* dm = nullptr;
+    float *dw = nullptr, *dp = nullptr;
+    CU(cudaMalloc((void**)&dc, sizeof(int) * (cells.size() + 1)));
+    CU(cudaMalloc((void**)&ds, sizeof(int) * start.size()));
+    CU(cudaMalloc((void**)&di, sizeof(int) * (sid.size() + 1)));
+    CU(cudaMalloc((void**)&dw, sizeof(float) * (wgt.size() + 1)));
+    CU(cudaMalloc((void**)&dp, sizeof(float) * N));
+    CU(cudaMalloc((void**)&dm, N));
+    pl->tr_cells.push_back(dc);
+    pl->tr_start.push_back(ds);
+    pl->tr_sid.push_back(di);
+    pl->tr_wgt.push_back(dw);
+    pl->tr_pw.push_back(dp);
+    pl->tr_mask.push_back(dm);
+    pl->tr_nnz.push_back((int)cells.size());
+    if (!cells.empty()) CU(cudaMemcpy(dc, cells.data(), sizeof(int) * cells.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ds, start.data(), sizeof(int) * start.size(), cudaMemcpyHostToDevice));
+    if (!sid.empty()) CU(cudaMemcpy(di, sid.data(), sizeof(int) * sid.size(), cudaMemcpyHostToDevice));
+    if (!wgt.empty()) CU(cudaMemcpy(dw, wgt.data(), sizeof(float) * wgt.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(dp, pw.data(), sizeof(float) * N, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(dm, m.data(), N, cudaMemcpyHostToDevice));
+  }
+  pl->traj_spokes = spokes;
+  pl->traj_turns = turns;
+  return NLINV_OK;
+}
+
 extern "C" nlinv_status nlinv_grid_radial(nlinv_plan pl, int frame, const nlinv_c32* raw, nlinv_c32* y, void* stream) {
   if (!pl || !raw || !y || frame < 0) return fail(pl, NLINV_ERR_ARG, "bad argument to nlinv_grid_radial");
   if (pl->traj_turns == 0) return fail(pl, NLINV_ERR_STATE, "nlinv_grid_radial before nlinv_plan_set_trajectory");
@@ -331,8 +434,17 @@ extern "C" nlinv_status nlinv_grid_radial(nlinv_plan pl, int frame, const nlinv_
   const int nraw = pl->traj_spokes * pl->ng;
   CU(cudaMemcpyAsync(pl->mask, pl->tr_mask[f], pl->N, cudaMemcpyDeviceToDevice, s));
   pl->mnnz_host = -1;
+  const bool kb = !pl->tr_wgt.empty();
+  if (kb) {   // KB gridding: the frame's real-valued P_k (R22), copied to a graph-stable buffer
+    if (!pl->pw_buf) CU(cudaMalloc((void**)&pl->pw_buf, sizeof(float) * pl->N));
+    CU(cudaMemcpyAsync(pl->pw_buf, pl->tr_pw[f], sizeof(float) * pl->N, cudaMemcpyDeviceToDevice, s));
+    pl->pw_active = pl->pw_buf;
+  } else {
+    pl->pw_active = nullptr;
+  }
   CU(launch_grid_radial(reinterpret_cast<const float2*>(raw), pl->J, nraw, pl->tr_cells[f], pl->tr_start[f],
-                        pl->tr_sid[f], pl->tr_nnz[f], pl->N, reinterpret_cast<float2*>(y), s));
+                        pl->tr_sid[f], kb ? pl->tr_wgt[f] : nullptr, pl->tr_nnz[f], pl->N,
+                        reinterpret_cast<float2*>(y), s));
   pl->launches += 1;
   return NLINV_OK;
 }
@@ -355,7 +467,10 @@ static void plan_free(nlinv_plan pl) {
   for (int* p : pl->tr_start) cudaFree(p);
   for (int* p : pl->tr_sid) cudaFree(p);
   for (uint8_t* p : pl->tr_mask) cudaFree(p);
+  for (float* p : pl->tr_wgt) cudaFree(p);
+  for (float* p : pl->tr_pw) cudaFree(p);
   cudaFree(pl->h_raw);
+  cudaFree(pl->pw_buf);
   if (pl->slab) {   // tA, tB, dx, r, p, c_omega live in the L2-persisting slab
     clear_access_window(pl->slab);
     cudaFree(pl->slab);
@@ -586,6 +701,7 @@ extern "C" nlinv_status nlinv_plan_set_mask(nlinv_plan pl, const uint8_t* mask_h
   for (size_t i = 0; i < pl->N; ++i) m8[i] = mask_host[i] ? 1 : 0;
   CU(cudaMemcpy(pl->mask, m8.data(), pl->N, cudaMemcpyHostToDevice));
   pl->mnnz_host = -1;
+  pl->pw_active = nullptr;   // a binary P_k replaces any KB weights
   return NLINV_OK;
 }
 
@@ -593,6 +709,7 @@ extern "C" nlinv_status nlinv_plan_set_mask_device(nlinv_plan pl, const uint8_t*
   if (!pl || !mask_dev) return fail(pl, NLINV_ERR_ARG, "NULL argument");
   CU(cudaMemcpyAsync(pl->mask, mask_dev, pl->N, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
   pl->mnnz_host = -1;
+  pl->pw_active = nullptr;
   return NLINV_OK;
 }
 
@@ -649,6 +766,7 @@ struct Enq {
     a.rho_spread = pl->rho_spread ? 1 : 0;
     a.winv = pl->winv;
     a.mask = pl->mask;
+    a.pw = pl->pw_active;
     a.scal = pl->scal;
     a.scal_w = pl->scal;
     a.counter = pl->counter;
@@ -877,7 +995,7 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
     TRY(q.kern("init_x", [&] { return launch_init_x(pl->xref, (long long)N, (long long)tot, q.s); }));
     TRY(q.kern("init_x", [&] { return launch_init_x(x, (long long)N, (long long)tot, q.s); }));
   }
-  if (pl->use_frame && K > 0) {
+  if (pl->use_frame && K > 0 && !pl->pw_active) {   // the frame kernel knows only the binary P_k
     // one cooperative launch for the whole frame (all Newton steps, CG iterations, output)
     FrameArgs f{};
     f.x = x;
@@ -1183,6 +1301,7 @@ static nlinv_status reconstruct_on(nlinv_plan pl, const nlinv_c32* frame, const 
   key.K = newton_steps;
   key.L = cg_iters;
   key.stream = s;
+  key.pw = pl->pw_active;
   const bool use_graph = (s != nullptr) && !pl->prof && (std::getenv("NLINV_NO_GRAPH") == nullptr);
   if (pl->gexec_valid_reset && pl->gexec) {
     cudaGraphExecDestroy(pl->gexec);
@@ -1290,6 +1409,7 @@ extern "C" nlinv_status nlinv_stream_frame(nlinv_plan pl, const nlinv_c32* frame
   CU(cudaMemcpyAsync(pl->h_frame, frame_host, sizeof(float2) * N * pl->J, cudaMemcpyHostToDevice, s));
   if (mask_host) {
     CU(cudaMemcpyAsync(pl->mask, mask_host, N, cudaMemcpyHostToDevice, s));
+    pl->pw_active = nullptr;   // a binary P_k from the host replaces any KB weights
     pl->mnnz_host = -1;
   }
   nlinv_status st = nlinv_reconstruct(pl, (const nlinv_c32*)pl->h_frame,
@@ -1429,6 +1549,7 @@ extern "C" nlinv_status nlinv_stream_frame_compact(nlinv_plan pl, const nlinv_c3
     long long cnt = 0;
     for (size_t i = 0; i < N; ++i) cnt += mask_host[i] ? 1 : 0;
     CU(cudaMemcpyAsync(pl->mask, mask_host, N, cudaMemcpyHostToDevice, s));
+    pl->pw_active = nullptr;   // a binary P_k from the host replaces any KB weights
     CU(launch_mask_compact(pl->mask, (int)N, pl->mcount, pl->midx, pl->mnnz, s));
     pl->launches += 2;
     pl->mnnz_host = cnt;

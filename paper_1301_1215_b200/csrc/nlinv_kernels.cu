@@ -292,34 +292,39 @@ cudaError_t launch_scatter_samples(const float2* samples, const int* idx, const 
   return launch_k(scatter_samples_kernel, dim3(148 * 4), dim3(256), 0, s, samples, idx, nnz, nnz_cap, J, N, y);
 }
 
-// GPU gridding of radial spokes (reading R20; "initial interpolation of the data to
-// the grid"): one thread per (coil, sampled cell); the cell's samples (CSR list built at
-// nlinv_plan_set_trajectory, ascending (spoke, readout) order) are averaged into y_j[cell].
-// Cells off P_k are not written (R16: only P_k y enters the method).
+// GPU gridding of radial spokes ("initial interpolation of the data to the
+// grid"): one thread per (coil, sampled cell); the cell's samples (CSR list built at
+// nlinv_plan_set_trajectory[_kb], ascending (spoke, readout) order) are averaged into y_j[cell] --
+// plain mean for nearest-cell gridding (R20), Kaiser-Bessel-weighted mean sum h d / sum h with
+// the per-entry weights wgt for convolution gridding (R22). Cells off P_k are not written (R16).
 __global__ void grid_radial_kernel(const float2* __restrict__ raw, int J, int nraw, const int* __restrict__ cells,
-                                   const int* __restrict__ start, const int* __restrict__ sid, int nnz, size_t N,
-                                   float2* __restrict__ y) {
+                                   const int* __restrict__ start, const int* __restrict__ sid,
+                                   const float* __restrict__ wgt, int nnz, size_t N, float2* __restrict__ y) {
   pdl_wait();
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)J * nnz;
        t += (long long)gridDim.x * blockDim.x) {
     const int j = (int)(t / nnz), e = (int)(t % nnz);
     const int a = start[e], b = start[e + 1];
     float2 acc = make_float2(0.f, 0.f);
+    float den = 0.f;
     for (int u = a; u < b; ++u) {
       const float2 v = raw[(size_t)j * nraw + sid[u]];
-      acc.x += v.x;
-      acc.y += v.y;
+      const float w = wgt ? wgt[u] : 1.0f;
+      acc.x = fmaf(w, v.x, acc.x);
+      acc.y = fmaf(w, v.y, acc.y);
+      den += w;
     }
-    const float inv = 1.0f / (float)(b - a);
+    const float inv = 1.0f / den;
     y[(size_t)j * N + cells[e]] = make_float2(acc.x * inv, acc.y * inv);
   }
 }
 cudaError_t launch_grid_radial(const float2* raw, int J, int nraw, const int* cells, const int* start, const int* sid,
-                               int nnz, size_t N, float2* y, cudaStream_t s) {
+                               const float* wgt, int nnz, size_t N, float2* y, cudaStream_t s) {
   long long nb = ((long long)J * nnz + 255) / 256;
   if (nb > 148 * 8) nb = 148 * 8;
   if (nb < 1) nb = 1;
-  return launch_k(grid_radial_kernel, dim3((unsigned)nb), dim3(256), 0, s, raw, J, nraw, cells, start, sid, nnz, N, y);
+  return launch_k(grid_radial_kernel, dim3((unsigned)nb), dim3(256), 0, s, raw, J, nraw, cells, start, sid, wgt, nnz, N,
+                  y);
 }
 
 cudaError_t launch_init_x(float2* x, long long nrho, long long ntot, cudaStream_t s) {

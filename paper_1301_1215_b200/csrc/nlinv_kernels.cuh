@@ -54,6 +54,7 @@ struct ColArgs {
   const float2* src2;      // second operand (chat_ref for RHS, p for NORMAL)
   const float* winv;       // [ng][ng]
   const uint8_t* mask;     // [ng][ng] P_k
+  const float* pw;         // [ng][ng] real-valued P_k = sqrt(PSF) of KB gridding (R22); nullptr = binary mask
   const float2* y;         // frame [J][ng][ng]
   float2* r;               // CG residual (chat blocks)
   float2* p;               // CG direction (chat blocks)
@@ -177,7 +178,7 @@ cudaError_t launch_mask_compact(const uint8_t* mask, int N, int* counts, int* id
 int mask_count_blocks(int N);
 cudaError_t launch_dx_side(const VecArgs& a, cudaStream_t s);
 cudaError_t launch_grid_radial(const float2* raw, int J, int nraw, const int* cells, const int* start, const int* sid,
-                               int nnz, size_t N, float2* y, cudaStream_t s);
+                               const float* wgt, int nnz, size_t N, float2* y, cudaStream_t s);
 cudaError_t launch_scatter_samples(const float2* samples, const int* idx, const int* nnz, int nnz_cap, int J,
                                    size_t N, float2* y, cudaStream_t s);
 bool col_fusable(int ng, int J);

@@ -75,6 +75,7 @@ _SIGS = {
     "nlinv_plan_trace": (c_int, [c_void_p, c_int, c_void_p, c_int]),
     "nlinv_plan_profile_json": (c_int, [c_void_p, ctypes.c_char_p, ctypes.c_size_t]),
     "nlinv_plan_set_trajectory": (c_int, [c_void_p, c_int, c_int]),
+    "nlinv_plan_set_trajectory_kb": (c_int, [c_void_p, c_int, c_int, ctypes.c_double, ctypes.c_double]),
     "nlinv_grid_radial": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
     "nlinv_stream_frame_radial": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p]),
     "nlinv_pca_create": (c_int, [c_int, c_int, ctypes.POINTER(c_void_p)]),
@@ -303,10 +304,18 @@ class Plan:
                                                int(newton_steps), int(cg_iters), ip, _stream_ptr(stream)), self._h)
         return image_out
 
-    def set_trajectory(self, spokes: int, turns: int):
-        """Radial trajectory for GPU gridding (R12 cells, R20 mean per cell)."""
+    def set_trajectory(self, spokes: int, turns: int, kernel: str = "nearest", width: float = 4.0,
+                       beta: float = 0.0):
+        """Radial trajectory for GPU gridding: kernel="nearest" (R12 cells, R20 mean per cell) or
+        "kb" (Kaiser-Bessel convolution gridding with a real-valued P_k = sqrt(PSF), R22)."""
         self.spokes, self.turns = int(spokes), int(turns)
-        _check(_lib.nlinv_plan_set_trajectory(self._h, self.spokes, self.turns), self._h)
+        if kernel == "nearest":
+            _check(_lib.nlinv_plan_set_trajectory(self._h, self.spokes, self.turns), self._h)
+        elif kernel == "kb":
+            _check(_lib.nlinv_plan_set_trajectory_kb(self._h, self.spokes, self.turns, float(width), float(beta)),
+                   self._h)
+        else:
+            raise ValueError("kernel must be 'nearest' or 'kb'")
 
     def grid_radial(self, frame: int, raw, y=None, stream=None):
         """Grid raw radial samples (CUDA complex64 [count, spokes, ng]) of frame `frame` into y
