@@ -333,9 +333,12 @@ def oracle_sample(cg_iters=CG):
     P = O.radial_mask(NG, SPOKES, TURNS, 0).astype(np.float64)
     winv, M = O.weights_inv(NG), O.fov_mask(NG)
     x0 = O.initial_x(J, NG)
-    t0 = time.perf_counter()
-    O.newton_step(x0, x0, y, P, winv, M, 1.0, cg_iters)
-    return time.perf_counter() - t0
+    # one host core, as reported ("cores": 1): BLAS / OpenMP pools limited to a single thread
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        O.newton_step(x0, x0, y, P, winv, M, 1.0, cg_iters)
+        return time.perf_counter() - t0
 
 
 def run_reference(args):
