@@ -27,7 +27,7 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 from paper_1301_1215_b200 import Plan, radial_mask  # noqa: E402
 
-NG, SPOKES, TURNS, NEWTON, CG, PERIOD = 384, 15, 5, 7, 10, 25
+PERIOD = 25
 
 
 def pct(v, q):
@@ -40,9 +40,16 @@ def main():
     ap.add_argument("--coils", type=int, default=32)
     ap.add_argument("--frames", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--ng", type=int, default=384)
+    ap.add_argument("--spokes", type=int, default=15)
+    ap.add_argument("--turns", type=int, default=5)
+    ap.add_argument("--newton", type=int, default=7)
+    ap.add_argument("--cg", type=int, default=10)
     ap.add_argument("--compress", type=int, default=0,
                     help="PCA-compress the coils to this many channels on the GPU before each frame (P:241)")
     args = ap.parse_args()
+    global NG, SPOKES, TURNS, NEWTON, CG
+    NG, SPOKES, TURNS, NEWTON, CG = args.ng, args.spokes, args.turns, args.newton, args.cg
     J = args.coils
     t0 = time.perf_counter()
     frames, masks = [], []
@@ -112,7 +119,7 @@ def main():
         e2e.append((time.perf_counter() - a) * 1e3)
     wall = time.perf_counter() - w0
     out = {
-        "config": "C4 (1 GPU)", "ng": NG, "coils": J, "spokes": SPOKES, "turns": TURNS, "newton": NEWTON, "cg": CG,
+        "config": "C4 (1 GPU)" if (NG, J) == (384, 32) else "custom", "ng": NG, "coils": J, "spokes": SPOKES, "turns": TURNS, "newton": NEWTON, "cg": CG,
         "frames": args.frames, "warmup": args.warmup, "distinct_frames": PERIOD,
         "device": {"fps": round(args.frames / (total / 1e3), 2), "latency_ms_p50": round(pct(lat, 0.5), 4),
                    "latency_ms_p95": round(pct(lat, 0.95), 4), "latency_ms_max": round(max(lat), 4),
