@@ -152,7 +152,11 @@ nlinv_status nlinv_apply_normal(nlinv_plan plan, float alpha, const nlinv_c32* d
  * x_out:  device unknowns, receives x_K (the next frame's prior).
  * image_out: device [n][n] complex, crop_Omega(rho . sqrt(sum_j |c_j|^2)) of x_K (R13), or NULL.
  *         With world > 1 every rank receives the full image.
- * Limits: 1 <= cg_iters <= 512, 0 <= newton_steps <= 64. */
+ * Limits: 1 <= cg_iters <= 512, 0 <= newton_steps <= 64.
+ * Execution: the frame is captured once into a CUDA graph per (buffers, K, L, P_k kind) and
+ * replayed; on the legacy default stream (stream == NULL) the graph runs on a plan-owned stream
+ * fenced by events on both sides, so the call stays ordered with `stream`. With a Kaiser-Bessel
+ * trajectory active (nlinv_plan_set_trajectory_kb + nlinv_grid_radial) P_k is real-valued (R22). */
 nlinv_status nlinv_reconstruct(nlinv_plan plan, const nlinv_c32* frame, const nlinv_c32* prior,
                                int newton_steps, int cg_iters, nlinv_c32* x_out, nlinv_c32* image_out,
                                void* stream);
