@@ -164,6 +164,118 @@ struct DFT<16, DIR> {
   __device__ __forceinline__ static void run(float2* a) { dft_split<4, 4, DIR>(a); }
 };
 
+// ------------------------------------------------------------------ zero-aware DFTs (pass 0 pruning)
+// Pass 0 of a transform whose input is known zero on fixed register slots (the Omega-pruned half
+// images: rows / columns outside Omega are structurally zero) skips the additions with those zeros:
+// bit n of ZM marks input n of the small DFT as zero (compile time). Adding a literal 0 cannot be
+// folded by the compiler under IEEE rules (-0 + 0 = +0), so this is done by hand.
+template <bool ZA, bool ZB>
+__device__ __forceinline__ float2 zadd(float2 a, float2 b) {
+  if constexpr (ZA && ZB) return make_float2(0.f, 0.f);
+  else if constexpr (ZA) return b;
+  else if constexpr (ZB) return a;
+  else return cadd(a, b);
+}
+template <bool ZA, bool ZB>
+__device__ __forceinline__ float2 zsub(float2 a, float2 b) {
+  if constexpr (ZA && ZB) return make_float2(0.f, 0.f);
+  else if constexpr (ZA) return make_float2(-b.x, -b.y);
+  else if constexpr (ZB) return a;
+  else return csub(a, b);
+}
+
+template <int R, int DIR, unsigned ZM>
+struct DFTZ {   // generic fallback: no pruning unless every input is zero
+  __device__ __forceinline__ static void run(float2* a) {
+    if constexpr (ZM != (1u << R) - 1u) DFT<R, DIR>::run(a);
+  }
+};
+template <int DIR, unsigned ZM>
+struct DFTZ<2, DIR, ZM> {
+  __device__ __forceinline__ static void run(float2* a) {
+    constexpr bool z0 = ZM & 1u, z1 = (ZM >> 1) & 1u;
+    const float2 t = a[0];
+    a[0] = zadd<z0, z1>(t, a[1]);
+    a[1] = zsub<z0, z1>(t, a[1]);
+  }
+};
+template <int DIR, unsigned ZM>
+struct DFTZ<4, DIR, ZM> {
+  __device__ __forceinline__ static void run(float2* a) {
+    constexpr bool z0 = ZM & 1u, z1 = (ZM >> 1) & 1u, z2 = (ZM >> 2) & 1u, z3 = (ZM >> 3) & 1u;
+    constexpr bool zt0 = z0 && z2, zt2 = z1 && z3;
+    const float2 t0 = zadd<z0, z2>(a[0], a[2]);
+    const float2 t1 = zsub<z0, z2>(a[0], a[2]);
+    const float2 t2 = zadd<z1, z3>(a[1], a[3]);
+    const float2 t3 = mul_dir_i<DIR>(zsub<z1, z3>(a[1], a[3]));
+    a[0] = zadd<zt0, zt2>(t0, t2);
+    a[2] = zsub<zt0, zt2>(t0, t2);
+    a[1] = zadd<zt0, zt2>(t1, t3);
+    a[3] = zsub<zt0, zt2>(t1, t3);
+  }
+};
+// group mask of the n2-th stride-R2 subsequence (n = R2 n1 + n2) of a length-R1*R2 input
+template <int R1, int R2>
+__host__ __device__ constexpr unsigned split_group_mask(unsigned zm, int n2) {
+  unsigned g = 0;
+  for (int n1 = 0; n1 < R1; ++n1) g |= ((zm >> (R2 * n1 + n2)) & 1u) << n1;
+  return g;
+}
+template <int R1, int R2>
+__host__ __device__ constexpr unsigned split_second_mask(unsigned zm) {
+  unsigned g = 0;
+  for (int n2 = 0; n2 < R2; ++n2) g |= (split_group_mask<R1, R2>(zm, n2) == (1u << R1) - 1u ? 1u : 0u) << n2;
+  return g;
+}
+template <int R1, int R2, int DIR, unsigned ZM, int N2>
+__device__ __forceinline__ void dftz_split_first(float2* a, float2* b) {
+  if constexpr (N2 < R2) {
+    constexpr int R = R1 * R2;
+    constexpr unsigned g = split_group_mask<R1, R2>(ZM, N2);
+    float2 t[R1];
+#pragma unroll
+    for (int n1 = 0; n1 < R1; ++n1) t[n1] = a[R2 * n1 + N2];
+    DFTZ<R1, DIR, g>::run(t);
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) {
+      if constexpr (g == (1u << R1) - 1u) b[N2 * R1 + k1] = make_float2(0.f, 0.f);
+      else b[N2 * R1 + k1] = mul_root48<DIR>(t[k1], ((N2 * k1) % R) * (48 / R));
+    }
+    dftz_split_first<R1, R2, DIR, ZM, N2 + 1>(a, b);
+  }
+}
+template <int R1, int R2, int DIR, unsigned ZM>
+__device__ __forceinline__ void dftz_split(float2* a) {
+  constexpr unsigned m2 = split_second_mask<R1, R2>(ZM);
+  float2 b[R1 * R2];
+  dftz_split_first<R1, R2, DIR, ZM, 0>(a, b);
+#pragma unroll
+  for (int k1 = 0; k1 < R1; ++k1) {
+    float2 t[R2];
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) t[n2] = b[n2 * R1 + k1];
+    DFTZ<R2, DIR, m2>::run(t);
+#pragma unroll
+    for (int k2 = 0; k2 < R2; ++k2) a[k1 + R1 * k2] = t[k2];
+  }
+}
+template <int DIR, unsigned ZM>
+struct DFTZ<6, DIR, ZM> {
+  __device__ __forceinline__ static void run(float2* a) { dftz_split<2, 3, DIR, ZM>(a); }
+};
+template <int DIR, unsigned ZM>
+struct DFTZ<8, DIR, ZM> {
+  __device__ __forceinline__ static void run(float2* a) { dftz_split<2, 4, DIR, ZM>(a); }
+};
+template <int DIR, unsigned ZM>
+struct DFTZ<12, DIR, ZM> {
+  __device__ __forceinline__ static void run(float2* a) { dftz_split<4, 3, DIR, ZM>(a); }
+};
+template <int DIR, unsigned ZM>
+struct DFTZ<16, DIR, ZM> {
+  __device__ __forceinline__ static void run(float2* a) { dftz_split<4, 4, DIR, ZM>(a); }
+};
+
 // ------------------------------------------------------------------ per-length schedules
 // R0 == R_last wherever possible so inverse->pointwise->forward stays in registers.
 template <int L>
@@ -266,10 +378,16 @@ __device__ __forceinline__ void pass_exchange(float2* v, int t, BUF& buf, SYNC s
 
 // Full length-L transform: registers in pass-0 input pattern -> registers in last-pass
 // output pattern. Unnormalised, X_k = sum_n x_n e^{DIR 2 pi i n k / L}.
-template <int L, int DIR, class BUF, class SYNC>
+// ZM0: bit r set if every register slot m*R0 + r of the pass-0 input is structurally zero
+template <int L, int DIR, unsigned ZM0 = 0, class BUF, class SYNC>
 __device__ __forceinline__ void fft(float2* v, int t, const float2* tw, BUF& buf, SYNC sync) {
   using C = Cfg<L>;
-  pass_compute<L, C::R0, 1, DIR>(v, t, tw);
+  if constexpr (ZM0 == 0) {
+    pass_compute<L, C::R0, 1, DIR>(v, t, tw);
+  } else {
+#pragma unroll
+    for (int m = 0; m < C::E / C::R0; ++m) DFTZ<C::R0, DIR, ZM0>::run(&v[m * C::R0]);
+  }
   pass_exchange<L, C::R0, 1, C::R1>(v, t, buf, sync);
   pass_compute<L, C::R1, C::R0, DIR>(v, t, tw);
   if constexpr (C::NP >= 3) {

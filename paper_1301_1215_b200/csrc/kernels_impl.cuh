@@ -94,6 +94,23 @@ __host__ __device__ constexpr int psh_out(int e) {
   return (e / R) * R + (e % R + R / 2) % R;
 }
 
+// Pass-0 zero masks (fft<..., ZM0>): bit r set if register slots m*R0 + r are structurally zero.
+// Omega-row / -column input (half images): positions outside [L/4, 3L/4) are zero.
+template <int L>
+__host__ __device__ constexpr unsigned omega_in_zmask() {
+  unsigned z = 0;
+  for (int r = 0; r < Cfg<L>::R0; ++r) {
+    const int pos = r * (L / Cfg<L>::R0);
+    if (pos < L / 4 || pos >= 3 * L / 4) z |= 1u << r;
+  }
+  return z;
+}
+// ... the same input after the half-shift register permutation (psh_in) of the row passes
+template <int L>
+__host__ __device__ constexpr unsigned omega_shift_zmask() {
+  return ((1u << Cfg<L>::R0) - 1u) & ~omega_in_zmask<L>();
+}
+
 // ------------------------------------------------------------------ deterministic reductions
 // Block sum in a fixed tree (warp xor-shuffles, then warps in index order). Result valid in
 // thread 0. red must hold 32 doubles.
@@ -487,7 +504,9 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
 
   if (tw_async) tw_wait();
   trace_stamp(a.trace, 1);
-  fft<L, DIR_FIRST>(v, t, tw, buf, SyncBlock{});
+  // half-image input modes: the rows outside Omega are zero (pass-0 pruning)
+  constexpr bool kHalfIn = !(MODE == CK_IFFT_W || MODE == CK_IFFT_W_CG || MODE == CK_ADJ1);
+  fft<L, DIR_FIRST, kHalfIn ? omega_in_zmask<L>() : 0u>(v, t, tw, buf, SyncBlock{});
   trace_stamp(a.trace, 2);
 
   // ---------------- middle: k-space pointwise (registers hold output pattern, index = k)
@@ -961,7 +980,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   if (pf_on) tw_wait_keep1();
   else tw_wait();
   trace_stamp(a.trace, 1);
-  fft<L, -1>(v, t, tw, buf, SyncBlock{});
+  fft<L, -1, omega_in_zmask<L>()>(v, t, tw, buf, SyncBlock{});   // T4: Omega rows only
   trace_stamp(a.trace, 2);
   if (pf_on) prefetch_wait();   // the r / dx tile is complete (all threads' copies)
 
@@ -1310,7 +1329,7 @@ __device__ __forceinline__ void row_task(const RowArgs& a, int pair0, const floa
     out_to_in<L>(v, t, buf, SyncWarp{});
 #pragma unroll
     for (int e = 0; e < E; ++e) w[e] = v[psh_in<L>(e)];   // half-shifted input of the row FFT
-    fft<L, -1>(w, t, tw, buf, SyncWarp{});
+    fft<L, -1, omega_shift_zmask<L>()>(w, t, tw, buf, SyncWarp{});   // Omega columns only
     if (active) {
 #pragma unroll
       for (int e = 0; e < E; ++e) {
@@ -1399,7 +1418,7 @@ __device__ __forceinline__ void row_task_k4(const RowArgs& a, int yy, int jlo, i
     out_to_in<L>(v, t, buf, SyncWarp{});
 #pragma unroll
     for (int e = 0; e < E; ++e) w[e] = v[psh_in<L>(e)];
-    fft<L, -1>(w, t, tw, buf, SyncWarp{});
+    fft<L, -1, omega_shift_zmask<L>()>(w, t, tw, buf, SyncWarp{});   // Omega columns only
     if (active) {
 #pragma unroll
       for (int e = 0; e < E; ++e) {
