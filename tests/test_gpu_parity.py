@@ -336,7 +336,8 @@ VARIANTS = {
 
 
 @pytest.mark.parametrize("variant", list(VARIANTS))
-@pytest.mark.parametrize("ng,J,spokes,turns,K,L", [(64, 6, 11, 1, 2, 6), (384, 12, 15, 5, 1, 4)])
+@pytest.mark.parametrize("ng,J,spokes,turns,K,L", [(64, 6, 11, 1, 2, 6), (384, 12, 15, 5, 1, 4), (32, 4, 8, 1, 2, 3),
+                                                    (32, 3, 8, 1, 2, 2)])
 def test_execution_variants_match_oracle(variant, ng, J, spokes, turns, K, L):
     """Every execution path of the library (read from the environment at plan creation) gives
     the oracle's frame: the fused cooperative passes, the unfused multi-kernel path used for
