@@ -341,3 +341,87 @@ def test_reconstruction_quality_c1():
         return np.linalg.norm(s * a - img) / np.linalg.norm(img)
 
     assert err(rec) < err(zf)
+
+
+# ---------------------------------------------------------------- frame output image_from_x (A13 / R13)
+# image = crop_Omega( rho . sqrt(sum_j |c_j|^2) ), c_j = F_c^H (w^-1 chat_j). Three pins that do not
+# reuse the oracle's own formula: a closed form, a marker pixel (crop geometry) and a term-by-term sum.
+def test_image_from_x_dc_closed_form():
+    # chat_j = a_j delta_DC  =>  c_j == a_j w^-1(0) / ng = a_j / ng  (w^-1(DC) = 1, unitary F_c), so
+    # image == crop(rho) * sqrt(sum_j |a_j|^2) / ng exactly. Catches: missing sqrt (sum |a|^2 / ng^2),
+    # rho only (no RSS factor), sum |c_j| instead of RSS (sum |a_j| / ng), conj / |rho| instead of rho.
+    ng, J = 16, 3
+    a = np.array([3.0 + 4.0j, -1.0 + 2.0j, 0.5 - 2.5j])
+    x = np.zeros((J + 1, ng, ng), complex)
+    x[0] = synth.random_complex(41, (ng, ng))
+    for j in range(J):
+        x[1 + j, ng // 2, ng // 2] = a[j]
+    q, n = ng // 4, ng // 2
+    want = x[0, q:q + n, q:q + n] * math.sqrt(sum(abs(v) ** 2 for v in a)) / ng
+    got = O.image_from_x(x)
+    assert got.shape == (n, n)
+    assert rel(got, want) < 1e-13
+
+
+def test_image_from_x_crop_marker():
+    # a single marker pixel of rho at (ng/4, ng/4) (the first Omega pixel) lands at image[0, 0];
+    # catches an off-by-one / transposed crop. RSS is made constant by DC-only coils.
+    ng, J = 16, 2
+    x = np.zeros((J + 1, ng, ng), complex)
+    x[0, ng // 4, ng // 4] = 2.0 - 1.0j
+    x[0, ng // 4 + 1, ng // 4 + 3] = 0.25j    # second marker: row 1, column 3 of the image
+    x[1, ng // 2, ng // 2] = 1.0
+    x[2, ng // 2, ng // 2] = 1.0j
+    got = O.image_from_x(x)
+    want = np.zeros((ng // 2, ng // 2), complex)
+    want[0, 0] = (2.0 - 1.0j) * math.sqrt(2.0) / ng
+    want[1, 3] = 0.25j * math.sqrt(2.0) / ng
+    assert np.allclose(got, want, rtol=0, atol=1e-15)
+
+
+def test_image_from_x_term_by_term():
+    # ng = 8, J = 2: c_j summed term by term from the centred DFT definition and the w^-1 closed form,
+    # then rho * sqrt(|c_1|^2 + |c_2|^2) pixel by pixel over the Omega crop
+    ng, J = 8, 2
+    x = synth.random_complex(43, (J + 1, ng, ng))
+    c0 = ng // 2
+    a_s, b_s = 220.0, 32.0
+    want = np.zeros((ng // 2, ng // 2), complex)
+    for yy in range(ng // 4, 3 * ng // 4):
+        for xx in range(ng // 4, 3 * ng // 4):
+            ss = 0.0
+            for j in range(J):
+                cj = 0.0 + 0.0j
+                for ky in range(ng):
+                    for kx in range(ng):
+                        kk = ((ky - c0) ** 2 + (kx - c0) ** 2) / ng ** 2
+                        w = (1.0 + a_s * kk) ** (-b_s / 2.0)
+                        cj += w * x[1 + j, ky, kx] * np.exp(2j * np.pi * ((ky - c0) * (yy - c0) + (kx - c0) * (xx - c0)) / ng)
+                cj /= ng
+                ss += abs(cj) ** 2
+            want[yy - ng // 4, xx - ng // 4] = x[0, yy, xx] * math.sqrt(ss)
+    assert rel(O.image_from_x(x), want) < 1e-12
+
+
+@pytest.mark.parametrize("kind", ["no_sqrt", "rho_only", "sum_abs", "crop_off_by_one", "conj_rho"])
+def test_image_pins_catch_mutations(kind, monkeypatch):
+    # meta-check of the three pins above: each plausible mistake in image_from_x fails at least one
+    import oracle.nlinv_oracle as ON
+
+    def mutant(x, prm=None):
+        ng = x.shape[-1]
+        c = ON.coils_from_chat(x[1:], ON.weights_inv(ng))
+        p2 = np.sum(np.abs(c) ** 2, axis=0)
+        rss = {"no_sqrt": p2, "rho_only": 1.0, "sum_abs": np.sum(np.abs(c), axis=0)}.get(kind, np.sqrt(p2))
+        img = (np.conj(x[0]) if kind == "conj_rho" else x[0]) * rss
+        q = ng // 4 + (1 if kind == "crop_off_by_one" else 0)
+        return img[q:q + ng // 2, q:q + ng // 2]
+
+    monkeypatch.setattr(O, "image_from_x", mutant)
+    caught = 0
+    for pin in (test_image_from_x_dc_closed_form, test_image_from_x_crop_marker, test_image_from_x_term_by_term):
+        try:
+            pin()
+        except AssertionError:
+            caught += 1
+    assert caught >= 1
