@@ -202,11 +202,6 @@ nlinv_status nlinv_stream_frame_compact(nlinv_plan plan, const nlinv_c32* sample
 nlinv_status nlinv_plan_set_profiling(nlinv_plan plan, int on);
 nlinv_status nlinv_plan_profile_json(nlinv_plan plan, char* buf, size_t len);
 
-/* Diagnostics of the persistent frame kernel: enable != 0 allocates/clears a timestamp buffer
- * (CTA 0 records %globaltimer after every grid barrier of later frames); enable == 0 copies up
- * to cap timestamps (ns) into out and their number into *count. */
-nlinv_status nlinv_plan_phase_times(nlinv_plan plan, int enable, unsigned long long* out, int cap, int* count);
-
 /* Debug (builds with -DNLV_TRACE only record data): col_mode >= 0 starts recording per-CTA
  * %globaltimer timelines (8 stamps per CTA) of the column pass with that internal mode;
  * col_mode < 0 copies up to cap stamps into out and stops recording. */

@@ -294,11 +294,7 @@ NLV_CFG(96, 24, 2, 12, 8, 1, 1)
 NLV_CFG(128, 16, 2, 16, 8, 1, 1)
 NLV_CFG(192, 24, 3, 8, 3, 8, 1)
 NLV_CFG(256, 16, 2, 16, 16, 1, 1)
-#ifdef NLV_E12_384
-NLV_CFG(384, 12, 4, 4, 4, 6, 4)
-#else
 NLV_CFG(384, 24, 3, 8, 6, 8, 1)
-#endif
 NLV_CFG(512, 16, 3, 8, 8, 8, 1)
 NLV_CFG(768, 24, 3, 8, 12, 8, 1)
 NLV_CFG(1024, 32, 3, 16, 4, 16, 1)

@@ -26,11 +26,7 @@ template <int L>
 struct ColGeo {
   static constexpr int T = Cfg<L>::T;
   static constexpr int c0 = (256 / T) < 32 ? (256 / T) : 32;
-#ifdef NLV_COLW   // experiment: force the column-tile width
-  static constexpr int CW = (NLV_COLW < c0) ? NLV_COLW : c0;
-#else
   static constexpr int CW = (L % c0 == 0) ? c0 : ((L % 16 == 0 && c0 >= 16) ? 16 : 8);
-#endif
   static constexpr int THREADS = CW * T;
   static constexpr size_t SMEM = sizeof(float2) * (size_t)L * (CW + 1) + 64 * sizeof(double);
   static constexpr size_t SMEM_PF = SMEM + 64 * sizeof(double) + sizeof(float2) * (size_t)L * CW;   // k5cg_kernel
@@ -163,28 +159,6 @@ __device__ __forceinline__ void grid_finish(const double (&v)[NV], double* parti
   }
 }
 
-// Sense-reversing barrier over nb co-resident CTAs (cooperative launch guarantees residency).
-__device__ __forceinline__ void grid_barrier_n(unsigned* count, unsigned* gen, unsigned nb) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned g = *(volatile unsigned*)gen;
-    __threadfence();
-    if (atomicAdd(count, 1u) == nb - 1) {
-      *count = 0u;
-      __threadfence();
-      atomicAdd(gen, 1u);
-    } else {
-      unsigned spins = 0;
-      while (*(volatile unsigned*)gen == g) {
-        __nanosleep(20);
-        if (++spins > (1u << 28)) __trap();  // never hang the GPU: abort the context instead
-      }
-    }
-    __threadfence();  // acquire; gpu-scope fence also invalidates this SM's L1
-  }
-  __syncthreads();
-}
-
 // Grid barrier with one atomic per CTA and no reset: CTA 0 adds 2^31 - (nb - 1), every other CTA
 // adds 1, so the word's top bit flips exactly when the last CTA arrives and the low bits return to
 // their value (reusable across launches and graph replays). Waiters poll with ld.acquire.gpu.
@@ -308,68 +282,10 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
   const int tid = threadIdx.x, c = tid % CW, t = tid / CW;
   const int x = tile * CW + c;
 
-  if constexpr (MODE == CK_IFFT_W_CG) {
-    if (j == a.J) {  // rho-block slice of the fused CG step (same update as the coil tiles below)
-      for (int y = rlo + t; y < rhi; y += T) {
-        const size_t i = (size_t)y * L + x;
-        float2 rv = a.rho_r[i];
-        const float2 pv = a.rho_p[i];
-        if (a.cg1 && a.iter > 0) {   // r_i = r_{i-1} - gamma A p_{i-1}
-          const float2 av = a.rho_a[i];
-          rv = make_float2(fmaf(-a.gamma, av.x, rv.x), fmaf(-a.gamma, av.y, rv.y));
-          a.rho_r[i] = rv;
-        }
-        if (a.iter > 0) {
-          const float2 dv = (a.iter > 1) ? a.rho_dx[i] : make_float2(0.f, 0.f);
-          a.rho_dx[i] = make_float2(fmaf(a.gamma, pv.x, dv.x), fmaf(a.gamma, pv.y, dv.y));
-        }
-        a.rho_p[i] = make_float2(fmaf(a.beta, pv.x, rv.x), fmaf(a.beta, pv.y, rv.y));
-      }
-      if (tw_async) asm volatile("cp.async.wait_all;\n" ::);
-      return;
-    }
-  }
-  if constexpr (MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ) {
-    if (j == a.J) {
-      // rho-block slice (replicated rho): out_rho = M . sum_s S_s (+ alpha p_rho | - alpha (rho - rho_ref))
-      const bool xin = (x >= q && x < q + n);
-      for (int y = rlo + t; y < rhi; y += T) {
-        const size_t i = (size_t)y * L + x;
-        float2 sv = make_float2(0.f, 0.f);
-        if (xin && y >= q && y < q + n) {
-          const size_t o = (size_t)(y - q) * n + (x - q);
-          for (int s = 0; s < a.nS; ++s) sv = cadd(sv, a.S[s * Qs + o]);   // ascending coil / rank order
-        }
-        if constexpr (MODE == CK_FFT_W_NORMAL) {
-          const float2 pv = a.rho_a[i];
-          const float2 o = make_float2(fmaf(a.alpha, pv.x, sv.x), fmaf(a.alpha, pv.y, sv.y));
-          a.rho_out[i] = o;
-          acc_rho += (double)pv.x * o.x + (double)pv.y * o.y;
-          if (a.cg1) {
-            const float2 rv = a.rho_r[i];
-            acc3[0] += (double)rv.x * o.x + (double)rv.y * o.y;
-            acc3[1] += (double)o.x * o.x + (double)o.y * o.y;
-            acc3[2] += (double)rv.x * rv.x + (double)rv.y * rv.y;
-          }
-        } else if constexpr (MODE == CK_FFT_W_RHS) {
-          const float2 d = csub(a.rho_a[i], a.rho_b[i]);
-          const float2 b = make_float2(fmaf(-a.alpha, d.x, sv.x), fmaf(-a.alpha, d.y, sv.y));
-          a.rho_r[i] = b;
-          a.rho_p[i] = b;
-          acc_rho += (double)b.x * b.x + (double)b.y * b.y;
-        } else {
-          a.rho_out[i] = sv;
-        }
-      }
-      if (tw_async) asm volatile("cp.async.wait_all;\n" ::);
-      return;
-    }
-  }
-
-  // rho block spread over the coil tiles (a.rho_spread): tile (j, tile) also handles a contiguous
-  // stripe of the N rho elements, so the pass needs no extra CTAs (one wave at 2 CTAs/SM)
+  // rho block spread over the coil tiles: tile (j, tile) also handles a contiguous stripe of the
+  // N rho elements, so the pass needs no extra CTAs (one wave at 2 CTAs/SM)
   if constexpr (MODE == CK_IFFT_W_CG || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ) {
-    if (a.rho_spread) {
+    {
       constexpr int NTILE = L / CW;
       const int nstripe = a.J * NTILE, stripe = j * NTILE + tile;
       const size_t chunk = (N + nstripe - 1) / nstripe;
@@ -597,8 +513,7 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
         if constexpr (MODE == CK_FFT_W_NORMAL) {
           const float2 pv = o1[u];
           const float2 o = make_float2(fmaf(a.alpha, pv.x, val.x), fmaf(a.alpha, pv.y, val.y));
-          if (a.fuse_update) v[e0 + u] = o;   // A p stays in registers for the fused r update
-          else a.out[j * N + i] = o;
+          a.out[j * N + i] = o;
           acc += (double)pv.x * o.x + (double)pv.y * o.y;
           if (a.cg1) {
             const float2 rv = o2[u];
@@ -615,163 +530,6 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
           acc += (double)b.x * b.x + (double)b.y * b.y;
         } else {
           a.out[j * N + i] = val;
-        }
-      }
-    }
-    if constexpr (MODE == CK_FFT_W_NORMAL) {
-      if (a.fuse_update) {
-        // K5 + CG residual update in one cooperative pass (world == 1): publish <p,Ap>, grid
-        // barrier, every CTA forms gamma from the partials in CTA order, then r -= gamma Ap on
-        // its own tile (A p still in registers) and its rho stripe; <r,r> goes to the last CTA.
-        const unsigned nb = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
-        double* sred = reinterpret_cast<double*>(xb);   // the exchange buffer is free here
-        __syncthreads();
-        trace_stamp(a.trace, 7);
-        const double pr = block_sum(acc_rho, sred);
-        const double pc = block_sum(acc, sred);
-        if (threadIdx.x == 0) {
-          a.fpart[2 * bid] = pr;
-          a.fpart[2 * bid + 1] = pc;
-        }
-        grid_barrier_n(a.bar_count, a.bar_gen, nb);
-        trace_stamp(a.trace, 3);
-        double tr = 0.0, tc = 0.0;
-        for (unsigned b = threadIdx.x; b < nb; b += blockDim.x) {
-          tr += __ldcg(a.fpart + 2 * b);
-          tc += __ldcg(a.fpart + 2 * b + 1);
-        }
-        tr = block_sum(tr, sred);
-        tc = block_sum(tc, sred);
-        __shared__ double s_pap[2];
-        if (threadIdx.x == 0) {
-          s_pap[0] = tr;
-          s_pap[1] = tc;
-          if (bid == 0) {
-            a.scal_w[SC_PAP_RHO + a.iter] = tr;
-            a.scal_w[SC_PAP_CHAT + a.iter] = tc;
-          }
-        }
-        __syncthreads();
-        const double rr = cg_rr(a.scal, a.iter);
-        const float gamma = (rr != 0.0) ? (float)(rr / (s_pap[0] + s_pap[1])) : 0.0f;
-        constexpr int NTILE = L / CW;
-        const int nstripe = a.J * NTILE, stripe = j * NTILE + tile;
-        const size_t chunk = (N + nstripe - 1) / nstripe;
-        const size_t lo = (size_t)stripe * chunk, hi = (lo + chunk < N) ? lo + chunk : N;
-        if (a.last_iter) {
-          if (a.fuse_newton) {
-            // Newton update x_{n+1} = x_n + dx + gamma_{L-1} p_{L-1} (Eq. 3) on this tile and stripe
-            const bool hasdx = a.iter > 0;
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-              const size_t i = j * N + (size_t)S::out_idx(t, e) * L + x;
-              const float2 pv = a.src2[i];
-              const float2 dv = hasdx ? a.dx[i] : make_float2(0.f, 0.f);
-              float2 xv = a.xc[i];
-              xv.x += fmaf(gamma, pv.x, dv.x);
-              xv.y += fmaf(gamma, pv.y, dv.y);
-              a.xc[i] = xv;
-            }
-            for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-              const float2 pv = a.rho_a[i];
-              const float2 dv = hasdx ? a.rho_dx[i] : make_float2(0.f, 0.f);
-              float2 xv = a.x_rho[i];
-              xv.x += fmaf(gamma, pv.x, dv.x);
-              xv.y += fmaf(gamma, pv.y, dv.y);
-              a.x_rho[i] = xv;
-            }
-          }
-        } else {
-          double ar = 0.0, ac = 0.0;
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const size_t i = j * N + (size_t)S::out_idx(t, e) * L + x;
-            float2 rv = a.r[i];
-            rv = make_float2(fmaf(-gamma, v[e].x, rv.x), fmaf(-gamma, v[e].y, rv.y));
-            a.r[i] = rv;
-            v[e] = rv;   // r_{i+1}, reused by the fused K1 below
-            ac += (double)rv.x * rv.x + (double)rv.y * rv.y;
-          }
-          for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-            const float2 av = a.rho_out[i];
-            float2 rv = a.rho_r[i];
-            rv = make_float2(fmaf(-gamma, av.x, rv.x), fmaf(-gamma, av.y, rv.y));
-            a.rho_r[i] = rv;
-            ar += (double)rv.x * rv.x + (double)rv.y * rv.y;
-          }
-          if (!a.fuse_k1) {
-            acc_rho = ar;   // handed back to the caller for the <r,r> last-CTA reduction
-            acc = ac;
-          } else {
-            // second barrier: <r_{i+1}, r_{i+1}> -> beta_i, then K1 of iteration i+1 on the same tile:
-            // dx += gamma_i p_i; p_{i+1} = r_{i+1} + beta_i p_i; t = w^-1 p_{i+1} -> column IFFT
-            const double rr_r = block_sum(ar, sred);
-            const double rr_c = block_sum(ac, sred);
-            if (threadIdx.x == 0) {
-              a.fpart[2 * nb + 2 * bid] = rr_r;
-              a.fpart[2 * nb + 2 * bid + 1] = rr_c;
-            }
-            grid_barrier_n(a.bar_count, a.bar_gen, nb);
-            trace_stamp(a.trace, 4);
-            double ur = 0.0, uc = 0.0;
-            for (unsigned b2 = threadIdx.x; b2 < nb; b2 += blockDim.x) {
-              ur += __ldcg(a.fpart + 2 * nb + 2 * b2);
-              uc += __ldcg(a.fpart + 2 * nb + 2 * b2 + 1);
-            }
-            ur = block_sum(ur, sred);
-            uc = block_sum(uc, sred);
-            __shared__ double s_rr[2];
-            if (threadIdx.x == 0) {
-              s_rr[0] = ur;
-              s_rr[1] = uc;
-              if (bid == 0) {
-                a.scal_w[SC_RR_RHO + a.iter + 1] = ur;
-                a.scal_w[SC_RR_CHAT + a.iter + 1] = uc;
-              }
-            }
-            __syncthreads();
-            const float beta = (rr != 0.0) ? (float)((s_rr[0] + s_rr[1]) / rr) : 0.0f;
-            const bool hasdx = a.iter > 0;
-            constexpr int CH = 8;
-#pragma unroll
-            for (int e0 = 0; e0 < E; e0 += CH) {
-              float wv[CH];
-              float2 pv[CH], dv[CH];
-#pragma unroll
-              for (int u = 0; u < CH; ++u) {
-                const size_t ii = (size_t)S::out_idx(t, e0 + u) * L + x;
-                wv[u] = a.winv[ii];
-                pv[u] = a.src2[j * N + ii];
-                dv[u] = hasdx ? a.dx[j * N + ii] : make_float2(0.f, 0.f);
-              }
-#pragma unroll
-              for (int u = 0; u < CH; ++u) {
-                const int k = S::out_idx(t, e0 + u);
-                const size_t i = j * N + (size_t)k * L + x;
-                a.dx[i] = make_float2(fmaf(gamma, pv[u].x, dv[u].x), fmaf(gamma, pv[u].y, dv[u].y));
-                const float2 pn = make_float2(fmaf(beta, pv[u].x, v[e0 + u].x), fmaf(beta, pv[u].y, v[e0 + u].y));
-                a.p[i] = pn;
-                v[e0 + u] = cscale(pn, wv[u] * sgn_of(k));
-              }
-            }
-            for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-              const float2 pv = a.rho_a[i], rv = a.rho_r[i];
-              const float2 dv = hasdx ? a.rho_dx[i] : make_float2(0.f, 0.f);
-              a.rho_dx[i] = make_float2(fmaf(gamma, pv.x, dv.x), fmaf(gamma, pv.y, dv.y));
-              a.rho_p[i] = make_float2(fmaf(beta, pv.x, rv.x), fmaf(beta, pv.y, rv.y));
-            }
-            __syncthreads();   // the reduction scratch (xb) becomes the transform's exchange buffer
-            out_to_in<L>(v, t, buf, SyncBlock{});
-            fft<L, +1>(v, t, tw, buf, SyncBlock{});
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-              if (out_is_omega<L>(e)) {
-                const int k = S::out_idx(t, e);
-                a.t1[j * H + (size_t)(k - q) * L + x] = cscale(v[e], invL * sgn_of(k));
-              }
-            }
-            acc_rho = acc = 0.0;
-          }
         }
       }
     }
@@ -834,20 +592,12 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColAr
     }
   }
   double acc_rho = 0.0, acc = 0.0;
-  // the rho slice (when present) is blockIdx.y == 0 so it is scheduled first
-  const bool has_rho = (MODE == CK_IFFT_W_CG || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ);
-  const int j = (has_rho && !a.rho_spread) ? (blockIdx.y == 0 ? a.J : (int)blockIdx.y - 1) : (int)blockIdx.y;
+  const int j = (int)blockIdx.y;
   double acc3[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};   // single-reduction CG dots (rho: 0-2, chat: 3-5)
   col_task<L, MODE, PW>(a, blockIdx.x, j, tw, xb, acc_rho, acc, acc3, 0, L, true, MODE == CK_PSF ? &mb : nullptr);
   trace_stamp(a.trace, 5);
   if constexpr (MODE == CK_RESADJ || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_NORMAL) {
-    if (MODE == CK_FFT_W_NORMAL && a.fuse_update) {
-      if (!a.last_iter && !a.fuse_k1) {  // <r_{i+1}, r_{i+1}> after the fused update
-        const double vv[2] = {acc_rho, acc};
-        const int sl[2] = {SC_RR_RHO + a.iter + 1, SC_RR_CHAT + a.iter + 1};
-        grid_finish<2>(vv, a.partials, a.counter, a.scal_w, sl, red);
-      }
-    } else if (MODE == CK_FFT_W_NORMAL && a.cg1 && a.partials != nullptr) {
+    if (MODE == CK_FFT_W_NORMAL && a.cg1 && a.partials != nullptr) {
       const double vv[8] = {acc_rho, acc, acc3[0], acc3[3], acc3[1], acc3[4], acc3[2], acc3[5]};
       const int sl[8] = {SC_PAP_RHO + a.iter, SC_PAP_CHAT + a.iter, SC_RAP_RHO + a.iter, SC_RAP_CHAT + a.iter,
                          SC_AA_RHO + a.iter,  SC_AA_CHAT + a.iter,  SC_RR_RHO + a.iter,  SC_RR_CHAT + a.iter};
@@ -1032,7 +782,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
       for (int ww = 0; ww < nw; ++ww) sk += red[8 + ww * NV + tid];
       a.fpart[tid * nb + bid] = sk;
     }
-    grid_sync_flip(a.bar_count + 2, nb, bid == 0);
+    grid_sync_flip(a.bar_count, nb, bid == 0);
     trace_stamp(a.trace, 3);
     // totals: warp w sums value k = w (+ nw ...) over all CTAs in a fixed order -> identical in every CTA
     for (int k = w; k < NV; k += nw) {
@@ -1101,10 +851,8 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
     return;
   }
 
-  // r_{i+1} = r - gamma Ap; dx += gamma p (unless dx_side); p_{i+1} = r_{i+1} + beta p (into p_out);
-  // t = w^-1 p_{i+1} (K1 prologue)
-  const bool dxs = a.dx_side != 0;
-  float2* pout = (a.p_out != nullptr) ? a.p_out : a.p;
+  // r_{i+1} = r - gamma Ap; dx += gamma p; p_{i+1} = r_{i+1} + beta p (in place); t = w^-1 p_{i+1}
+  // (K1 prologue)
   {
     constexpr int CH = 8;
 #pragma unroll
@@ -1115,7 +863,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
       for (int u = 0; u < CH; ++u) {
         const size_t ii = (size_t)S::out_idx(t, e0 + u) * L + x;
         wv[u] = a.winv[ii];
-        dv[u] = (hasdx && !dxs) ? a.dx[j * N + ii] : make_float2(0.f, 0.f);
+        dv[u] = hasdx ? a.dx[j * N + ii] : make_float2(0.f, 0.f);
       }
 #pragma unroll
       for (int u = 0; u < CH; ++u) {
@@ -1124,9 +872,9 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
         const float2 rv = pf[k * CW + c], pv = buf(k);
         const float2 rn = make_float2(fmaf(-gamma, v[e0 + u].x, rv.x), fmaf(-gamma, v[e0 + u].y, rv.y));
         a.r[i] = rn;
-        if (!dxs) a.dx[i] = make_float2(fmaf(gamma, pv.x, dv[u].x), fmaf(gamma, pv.y, dv[u].y));
+        a.dx[i] = make_float2(fmaf(gamma, pv.x, dv[u].x), fmaf(gamma, pv.y, dv[u].y));
         const float2 pn = make_float2(fmaf(beta, pv.x, rn.x), fmaf(beta, pv.y, rn.y));
-        pout[i] = pn;
+        a.p[i] = pn;
         v[e0 + u] = cscale(pn, wv[u] * sgn_of(k));
       }
     }
@@ -1135,10 +883,8 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   auto update_rho = [&](size_t i, float2 av, float2 rv, float2 pv) {
     const float2 rn = make_float2(fmaf(-gamma, av.x, rv.x), fmaf(-gamma, av.y, rv.y));
     a.rho_r[i] = rn;
-    if (!dxs) {
-      const float2 dv = hasdx ? a.rho_dx[i] : make_float2(0.f, 0.f);
-      a.rho_dx[i] = make_float2(fmaf(gamma, pv.x, dv.x), fmaf(gamma, pv.y, dv.y));
-    }
+    const float2 dv = hasdx ? a.rho_dx[i] : make_float2(0.f, 0.f);
+    a.rho_dx[i] = make_float2(fmaf(gamma, pv.x, dv.x), fmaf(gamma, pv.y, dv.y));
     a.rho_p[i] = make_float2(fmaf(beta, pv.x, rn.x), fmaf(beta, pv.y, rn.y));
   };
   if (sreg) {
@@ -1482,551 +1228,6 @@ __global__ void __launch_bounds__(256, NLV_MINB) row_kernel(RowArgs a, const flo
   }
 }
 
-// ------------------------------------------------------------------ persistent frame kernel
-// One cooperative launch runs a whole frame (all Newton steps, all CG iterations) with grid
-// barriers between the passes, so the ~7 kernel boundaries per CG iteration (each a launch,
-// ramp-up and drain) become barriers and the twiddle table stays resident in shared memory.
-// Reductions: every CTA publishes (rho, chat) partials; after the barrier every CTA sums all
-// partials in CTA order itself (deterministic, no extra pass). world == 1 only (no NCCL inside).
-
-// Sense-reversing grid barrier over co-resident CTAs (cooperative launch guarantees residency).
-__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned nb = gridDim.x;
-    const unsigned g = *(volatile unsigned*)gen;
-    __threadfence();
-    if (atomicAdd(count, 1u) == nb - 1) {
-      *count = 0u;
-      __threadfence();
-      atomicAdd(gen, 1u);
-    } else {
-      unsigned spins = 0;
-      while (*(volatile unsigned*)gen == g) {
-        __nanosleep(20);
-        if (++spins > (1u << 28)) __trap();  // never hang the GPU: abort the context instead
-      }
-    }
-    __threadfence();  // acquire; gpu-scope fence also invalidates this SM's L1
-  }
-  __syncthreads();
-}
-
-// Publish this CTA's (rho, chat) partials to slot, barrier, and return the ordered totals.
-__device__ __forceinline__ double2 grid_reduce2(double vr, double vc, double* red_slot, unsigned* count,
-                                                unsigned* gen, double* sred) {
-  const double sr = block_sum(vr, sred);
-  const double sc = block_sum(vc, sred);
-  if (threadIdx.x == 0) {
-    red_slot[2 * blockIdx.x] = sr;
-    red_slot[2 * blockIdx.x + 1] = sc;
-  }
-  grid_barrier(count, gen);
-  __shared__ double2 tot;
-  if (threadIdx.x < 32) {
-    double ar = 0.0, ac = 0.0;
-    const volatile double* rs = red_slot;
-    for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) {
-      ar += rs[2 * b];
-      ac += rs[2 * b + 1];
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      ar += __shfl_xor_sync(0xffffffffu, ar, o);
-      ac += __shfl_xor_sync(0xffffffffu, ac, o);
-    }
-    if (threadIdx.x == 0) tot = make_double2(ar, ac);
-  }
-  __syncthreads();
-  return tot;
-}
-
-// Publish NV per-CTA partials, barrier, return the CTA-ordered totals (every CTA computes them).
-template <int NV>
-__device__ __forceinline__ void grid_reduceN(const double (&v)[NV], double* red_slot, unsigned* count,
-                                             unsigned* gen, double* sred, double (&tot)[NV]) {
-  double s[NV];
-#pragma unroll
-  for (int k = 0; k < NV; ++k) s[k] = block_sum(v[k], sred);
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) red_slot[NV * blockIdx.x + k] = s[k];
-  }
-  grid_barrier(count, gen);
-  __shared__ double stot[8];
-  if (threadIdx.x < 32) {
-    double a[NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) a[k] = 0.0;
-    const volatile double* rs = red_slot;
-    for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) {
-#pragma unroll
-      for (int k = 0; k < NV; ++k) a[k] += rs[NV * b + k];
-    }
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) a[k] += __shfl_xor_sync(0xffffffffu, a[k], o);
-    }
-    if (threadIdx.x == 0) {
-#pragma unroll
-      for (int k = 0; k < NV; ++k) stot[k] = a[k];
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < NV; ++k) tot[k] = stot[k];
-  __syncthreads();
-}
-
-template <int L>
-struct FrameGeo {
-  static constexpr int NT = 256;
-  static constexpr bool kOk = (ColGeo<L>::THREADS == NT);  // 256-thread column tiles (ng >= 64, except 96)
-  static constexpr size_t SMEM_COL = sizeof(float2) * (size_t)L * ColGeo<L>::CW;
-  static constexpr size_t SMEM_ROW = sizeof(float2) * (size_t)L * RowGeo<L>::GPC + sizeof(float2) * (L / 2);
-  static constexpr size_t XB = SMEM_COL > SMEM_ROW ? SMEM_COL : SMEM_ROW;
-  static constexpr size_t SMEM = sizeof(float2) * L + XB + 64 * sizeof(double);
-};
-
-template <int L, int MODE>
-__device__ __forceinline__ void col_phase(const ColArgs& a, const float2* tw, float2* xb, int nslices,
-                                          double& acc_rho, double& acc, double* acc3) {
-  constexpr int NTILE = L / ColGeo<L>::CW;
-  const int ntask = NTILE * nslices;
-  for (int task = blockIdx.x; task < ntask; task += gridDim.x) {
-    // rho slice (j == J, when present) first: its tasks are longer than one coil tile
-    const int jj = task / NTILE, tile = task % NTILE;
-    const int j = (nslices > a.J) ? (jj == 0 ? a.J : jj - 1) : jj;
-    col_task<L, MODE>(a, tile, j, tw, xb, acc_rho, acc, acc3);
-    __syncthreads();  // the next task reuses xb
-  }
-}
-
-template <int L, int MODE>
-__device__ __forceinline__ void row_phase(const RowArgs& a, const float2* tw, float2* xb) {
-  constexpr int GPC = RowGeo<L>::GPC;
-  if constexpr (MODE == RK_K4) {
-    for (int yy = blockIdx.x; yy < L / 2; yy += gridDim.x)
-      row_task_k4<L>(a, yy, 0, a.J, 0, tw, xb, xb + (size_t)L * GPC);
-  } else {
-    const int ntask = (a.J * (L / 2) + GPC - 1) / GPC;
-    for (int task = blockIdx.x; task < ntask; task += gridDim.x) row_task<L, MODE>(a, task * GPC, tw, xb);
-  }
-}
-
-// ------------------------------------------------------------------ dataflow CG segment
-// Passes K1..K5 of one CG iteration as a task queue instead of five grid-wide phases: a task
-// waits only for the tasks of the same coil it reads from (per-coil completion counters), so
-// the passes of different coils overlap and no CTA idles at a grid barrier. Task order is
-// pass-major, every dependency points to an earlier ticket, so the queue cannot deadlock.
-__device__ __forceinline__ void wait_ge(const unsigned* ctr, unsigned target) {
-  unsigned spins = 0;
-  while (*(volatile const unsigned*)ctr < target) {
-    __nanosleep(40);
-    if (++spins > (1u << 28)) __trap();
-  }
-}
-
-__device__ __forceinline__ void task_done(unsigned* ctr) {
-  __syncthreads();  // every thread's stores of this task are issued
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
-  }
-}
-
-template <int L>
-__device__ __forceinline__ void cg_segment(const FrameArgs& f, ColArgs& ca, RowArgs& ra, const float2* tw,
-                                           float2* xb, double* sred, int g, float alpha) {
-  constexpr int NTILE = L / ColGeo<L>::CW;
-  constexpr int GPC = RowGeo<L>::GPC;
-  constexpr int NRB = (L / 2) / GPC;   // row tasks per coil
-  constexpr size_t N = (size_t)L * L;
-  const int J = f.J;
-  const unsigned gt = (unsigned)(g + 1);
-  unsigned* done = f.done;             // [5][J + 1] cumulative task completions
-  unsigned* qh = f.qhead + (g & 1);
-  const int n1 = NTILE * (J + 1), n2 = NRB * J, n3 = NTILE * J, n4 = NRB * J, n5 = NTILE * J, n5r = 4 * NTILE;
-  const int e1 = n1, e2 = e1 + n2, e3 = e2 + n3, e4 = e3 + n4, e5 = e4 + n5, e6 = e5 + n5r;
-  __shared__ int s_ticket;
-  for (;;) {
-    if (threadIdx.x == 0) s_ticket = (int)atomicAdd(qh, 1u);
-    __syncthreads();
-    const int tk = s_ticket;
-    __syncthreads();
-    if (tk >= e6) break;
-    double d0 = 0.0, d1 = 0.0, a3[4] = {0.0, 0.0, 0.0, 0.0};
-    if (tk < e1) {                                   // K1 (+ fused CG step); rho slice first
-      const int jj = tk / NTILE, tile = tk % NTILE;
-      const int j = (jj == 0) ? J : jj - 1;
-      ca.out = f.tA;
-      col_task<L, CK_IFFT_W_CG>(ca, tile, j, tw, xb, d0, d1, a3);
-      task_done(&done[0 * (J + 1) + j]);
-    } else if (tk < e2) {                            // K2
-      const int t2 = tk - e1, j = t2 / NRB, rb = t2 % NRB;
-      if (threadIdx.x == 0) {
-        wait_ge(&done[0 * (J + 1) + j], gt * NTILE);
-        wait_ge(&done[0 * (J + 1) + J], gt * NTILE);
-        __threadfence();
-      }
-      __syncthreads();
-      ra.in = f.tA;
-      ra.out = f.tB;
-      ra.prho = f.p;
-      row_task<L, RK_K2>(ra, j * (L / 2) + rb * GPC, tw, xb);
-      task_done(&done[1 * (J + 1) + j]);
-    } else if (tk < e3) {                            // K3
-      const int t3 = tk - e2, j = t3 / NTILE, tile = t3 % NTILE;
-      if (threadIdx.x == 0) {
-        wait_ge(&done[1 * (J + 1) + j], gt * NRB);
-        __threadfence();
-      }
-      __syncthreads();
-      ca.in = f.tB;
-      ca.out = f.tA;
-      col_task<L, CK_PSF>(ca, tile, j, tw, xb, d0, d1, a3);
-      task_done(&done[2 * (J + 1) + j]);
-    } else if (tk < e4) {                            // K4 (per-coil channel-sum terms)
-      const int t4 = tk - e3, j = t4 / NRB, rb = t4 % NRB;
-      if (threadIdx.x == 0) {
-        wait_ge(&done[2 * (J + 1) + j], gt * NTILE);
-        __threadfence();
-      }
-      __syncthreads();
-      ra.in = f.tA;
-      ra.out = f.tB;
-      ra.S = f.S_coils;
-      row_task<L, RK_K4>(ra, j * (L / 2) + rb * GPC, tw, xb);
-      task_done(&done[3 * (J + 1) + j]);
-    } else {                                         // K5 coil tiles, then the rho slice
-      const int t5 = tk - e4;
-      int j, tile, rlo = 0, rhi = L;
-      if (t5 < n5) {
-        j = t5 / NTILE;
-        tile = t5 % NTILE;
-        if (threadIdx.x == 0) {
-          wait_ge(&done[3 * (J + 1) + j], gt * NRB);
-          __threadfence();
-        }
-      } else {
-        j = J;
-        tile = (t5 - n5) % NTILE;
-        const int qq = (t5 - n5) / NTILE;
-        rlo = qq * (L / 4);
-        rhi = rlo + L / 4;
-        if (threadIdx.x == 0) {
-          for (int jj = 0; jj < J; ++jj) wait_ge(&done[3 * (J + 1) + jj], gt * NRB);
-          __threadfence();
-        }
-      }
-      __syncthreads();
-      ca.in = f.tB;
-      ca.src2 = f.p + N;
-      ca.out = f.Ap + N;
-      ca.rho_a = f.p;
-      ca.rho_out = f.Ap;
-      ca.S = f.S_coils;
-      ca.nS = J;
-      ca.alpha = alpha;
-      col_task<L, CK_FFT_W_NORMAL>(ca, tile, j, tw, xb, d0, d1, a3, rlo, rhi);
-      // per-task partials, summed later in task order (deterministic under dynamic scheduling)
-      const double sr = block_sum(d0, sred);
-      const double sc = block_sum(d1, sred);
-      if (threadIdx.x == 0) {
-        f.tred[2 * t5] = sr;
-        f.tred[2 * t5 + 1] = sc;
-      }
-      __syncthreads();
-    }
-  }
-}
-
-// Sum the per-task partials of the K5 tasks in task order (after a grid barrier).
-__device__ __forceinline__ double2 sum_task_partials(const double* tred, int ntask) {
-  __shared__ double2 tot;
-  if (threadIdx.x < 32) {
-    double ar = 0.0, ac = 0.0;
-    const volatile double* rs = tred;
-    for (int b = threadIdx.x; b < ntask; b += 32) {
-      ar += rs[2 * b];
-      ac += rs[2 * b + 1];
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      ar += __shfl_xor_sync(0xffffffffu, ar, o);
-      ac += __shfl_xor_sync(0xffffffffu, ac, o);
-    }
-    if (threadIdx.x == 0) tot = make_double2(ar, ac);
-  }
-  __syncthreads();
-  const double2 r = tot;
-  __syncthreads();
-  return r;
-}
-
-// optional phase timestamps (CTA 0, after each barrier) for the per-phase breakdown
-__device__ __forceinline__ void stamp(const FrameArgs& f, int& ns) {
-  if (f.tstamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && ns < f.tstamp_cap) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    f.tstamp[ns] = t;
-  }
-  ++ns;
-}
-
-template <int L>
-__global__ void __launch_bounds__(256, 2) frame_kernel(FrameArgs f) {
-  constexpr int n = L / 2;
-  constexpr size_t N = (size_t)L * L, Q = (size_t)n * n;
-  extern __shared__ float4 smem_raw[];
-  float2* tw = reinterpret_cast<float2*>(smem_raw);
-  float2* xb = tw + L;
-  double* sred = reinterpret_cast<double*>(reinterpret_cast<char*>(xb) + FrameGeo<L>::XB);
-  for (int i = threadIdx.x; i < L; i += blockDim.x) tw[i] = f.tw[i];
-  if (blockIdx.x == 0) {
-    for (int i = threadIdx.x; i < 5 * (f.J + 1); i += blockDim.x) f.done[i] = 0u;
-    if (threadIdx.x < 2) f.qhead[threadIdx.x] = 0u;
-  }
-  __syncthreads();
-  grid_barrier(f.bar_count, f.bar_gen);
-  int nstamp = 0;
-  stamp(f, nstamp);
-
-  const int J = f.J;
-  ColArgs ca{};
-  ca.winv = f.winv;
-  ca.mask = f.mask;
-  ca.y = f.y;
-  ca.J = J;
-  ca.S = f.S_all;
-  ca.nS = 1;
-  RowArgs ra{};
-  ra.J = J;
-  ra.c_omega = f.c_omega;
-  ra.rho_omega = f.rho_omega;
-  ra.S = f.S_all;
-  ra.rss = f.rss_all;
-
-  double alpha_d = f.alpha0;
-  for (int nstep = 0; nstep < f.K; ++nstep, alpha_d *= f.q) {
-    const float alpha = (float)alpha_d;
-    double d0 = 0.0, d1 = 0.0;
-    // N1: c_j = W^-1 chat_j, column half
-    ca.src = f.x + N;
-    ca.out = f.tA;
-    { double a3[4]; col_phase<L, CK_IFFT_W>(ca, tw, xb, J, d0, d1, a3); }
-    grid_barrier(f.bar_count, f.bar_gen);
-    stamp(f, nstamp);
-    // N2: row half of c_j, c|Omega, rho|Omega, and the row FFT of rho c_j (forward operator)
-    ra.in = f.tA;
-    ra.out = f.tB;
-    ra.xrho = f.x;
-    row_phase<L, RK_SETPOINT_FWD>(ra, tw, xb);
-    grid_barrier(f.bar_count, f.bar_gen);
-    stamp(f, nstamp);
-    // N3: column FFT -> r = P (y - F x) (+ ||r||^2) -> column IFFT (adjoint head)
-    ca.in = f.tB;
-    ca.out = f.tA;
-    d0 = d1 = 0.0;
-    { double a3[4]; col_phase<L, CK_RESADJ>(ca, tw, xb, J, d0, d1, a3); }
-    double2 res = grid_reduce2(d0, d1, f.red + 0 * 6 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
-    stamp(f, nstamp);
-    if (blockIdx.x == 0 && threadIdx.x == 0) f.scal[SC_RES + nstep] = res.y;
-    // N4: row IFFT -> u, ordered sum_j conj(c_j) u_j, conj(rho) u -> row FFT
-    ra.in = f.tA;
-    ra.out = f.tB;
-    ra.S = f.S_all;
-    row_phase<L, RK_K4>(ra, tw, xb);
-    grid_barrier(f.bar_count, f.bar_gen);
-    stamp(f, nstamp);
-    // N5: rhs b = DF^H r - alpha (x - x_ref); r = p = b
-    ca.in = f.tB;
-    ca.S = f.S_all;
-    ca.nS = 1;
-    ca.src = f.x + N;
-    ca.src2 = f.xref + N;
-    ca.r = f.r + N;
-    ca.p = f.p + N;
-    ca.rho_a = f.x;
-    ca.rho_b = f.xref;
-    ca.rho_r = f.r;
-    ca.rho_p = f.p;
-    ca.alpha = alpha;
-    d0 = d1 = 0.0;
-    { double a3[4]; col_phase<L, CK_FFT_W_RHS>(ca, tw, xb, J + 1, d0, d1, a3); }
-    double2 rr2 = grid_reduce2(d0, d1, f.red + 1 * 6 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
-    stamp(f, nstamp);
-    double acc3[6];
-    double rr = rr2.x + rr2.y;   // rr_0
-    float gamma = 0.0f, beta = 0.0f;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      f.scal[SC_RR_RHO] = rr2.x;
-      f.scal[SC_RR_CHAT] = rr2.y;
-    }
-    // CG: K1 also carries dx += gamma_{i-1} p_{i-1}; the update pass only updates r
-    for (int it = 0; it < f.L; ++it) {
-      double2 pap;
-      ca.r = f.r + N;
-      ca.p = f.p + N;
-      ca.dx = f.dx + N;
-      ca.rho_r = f.r;
-      ca.rho_p = f.p;
-      ca.rho_dx = f.dx;
-      ca.iter = it;
-      ca.gamma = gamma;
-      ca.beta = beta;
-      if (f.dataflow) {
-        // P1..P5 as a per-coil dataflow task queue, then one barrier for <p, Ap>
-        cg_segment<L>(f, ca, ra, tw, xb, sred, nstep * f.L + it, alpha);
-        grid_barrier(f.bar_count, f.bar_gen);
-        pap = sum_task_partials(f.tred, (L / ColGeo<L>::CW) * (J + 4));
-        if (blockIdx.x == 0 && threadIdx.x == 0) f.qhead[(nstep * f.L + it + 1) & 1] = 0u;
-        stamp(f, nstamp);
-      } else {
-        // P1: CG step (dx, p) fused with t = w^-1 p -> column IFFT
-        ca.out = f.tA;
-        col_phase<L, CK_IFFT_W_CG>(ca, tw, xb, J + 1, d0, d1, acc3);
-        grid_barrier(f.bar_count, f.bar_gen);
-        stamp(f, nstamp);
-        // P2: K2
-        ra.in = f.tA;
-        ra.out = f.tB;
-        ra.prho = f.p;
-        row_phase<L, RK_K2>(ra, tw, xb);
-        grid_barrier(f.bar_count, f.bar_gen);
-        stamp(f, nstamp);
-        // P3: K3 (PSF convolution)
-        ca.in = f.tB;
-        ca.out = f.tA;
-        col_phase<L, CK_PSF>(ca, tw, xb, J, d0, d1, acc3);
-        grid_barrier(f.bar_count, f.bar_gen);
-        stamp(f, nstamp);
-        // P4: K4
-        ra.in = f.tA;
-        ra.out = f.tB;
-        ra.S = f.S_all;
-        row_phase<L, RK_K4>(ra, tw, xb);
-        grid_barrier(f.bar_count, f.bar_gen);
-        stamp(f, nstamp);
-        // P5: K5 + rho slice: Ap, <p, Ap>
-        ca.in = f.tB;
-        ca.src2 = f.p + N;
-        ca.out = f.Ap + N;
-        ca.rho_a = f.p;
-        ca.rho_out = f.Ap;
-        ca.S = f.S_all;
-        ca.nS = 1;
-        ca.alpha = alpha;
-        d0 = d1 = 0.0;
-        col_phase<L, CK_FFT_W_NORMAL>(ca, tw, xb, J + 1, d0, d1, acc3);
-        pap = grid_reduce2(d0, d1, f.red + 2 * 6 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
-        stamp(f, nstamp);
-      }
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
-        f.scal[SC_PAP_RHO + it] = pap.x;
-        f.scal[SC_PAP_CHAT + it] = pap.y;
-      }
-      gamma = (rr != 0.0) ? (float)(rr / (pap.x + pap.y)) : 0.0f;
-      if (it < f.L - 1) {
-        // P6: r -= gamma Ap; <r, r>
-        const long long n2 = (long long)N * (J + 1) / 2, nrho2 = (long long)N / 2;
-        const long long stride = (long long)gridDim.x * blockDim.x;
-        float4* r4 = reinterpret_cast<float4*>(f.r);
-        const float4* ap4 = reinterpret_cast<const float4*>(f.Ap);
-        double ar = 0.0, ac = 0.0;
-        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += stride) {
-          const float4 av = ap4[i];
-          float4 rv = r4[i];
-          rv.x = fmaf(-gamma, av.x, rv.x); rv.y = fmaf(-gamma, av.y, rv.y);
-          rv.z = fmaf(-gamma, av.z, rv.z); rv.w = fmaf(-gamma, av.w, rv.w);
-          r4[i] = rv;
-          const double sq = (double)rv.x * rv.x + (double)rv.y * rv.y + (double)rv.z * rv.z + (double)rv.w * rv.w;
-          if (i < nrho2) ar += sq; else ac += sq;
-        }
-        const double2 r2 = grid_reduce2(ar, ac, f.red + 1 * 6 * kMaxFrameBlocks, f.bar_count, f.bar_gen, sred);
-        stamp(f, nstamp);
-        const double rr_next = r2.x + r2.y;
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-          f.scal[SC_RR_RHO + it + 1] = r2.x;
-          f.scal[SC_RR_CHAT + it + 1] = r2.y;
-        }
-        beta = (rr != 0.0) ? (float)(rr_next / rr) : 0.0f;
-        rr = rr_next;
-      }
-    }
-    // Newton update x_{n+1} = x_n + dx, with the last step's gamma p folded in (Eq. 3)
-    {
-      const long long n2 = (long long)N * (J + 1) / 2;
-      const long long stride = (long long)gridDim.x * blockDim.x;
-      const float4* p4 = reinterpret_cast<const float4*>(f.p);
-      const float4* dx4 = reinterpret_cast<const float4*>(f.dx);
-      float4* x4 = reinterpret_cast<float4*>(f.x);
-      const bool hasdx = f.L > 1;
-      for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += stride) {
-        const float4 pv = p4[i];
-        float4 d = hasdx ? dx4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-        float4 xv = x4[i];
-        xv.x += fmaf(gamma, pv.x, d.x); xv.y += fmaf(gamma, pv.y, d.y);
-        xv.z += fmaf(gamma, pv.z, d.z); xv.w += fmaf(gamma, pv.w, d.w);
-        x4[i] = xv;
-      }
-      grid_barrier(f.bar_count, f.bar_gen);
-      stamp(f, nstamp);
-    }
-  }
-  if (f.img != nullptr) {
-    double d0 = 0.0, d1 = 0.0;
-    ca.src = f.x + N;
-    ca.out = f.tA;
-    { double a3[4]; col_phase<L, CK_IFFT_W>(ca, tw, xb, J, d0, d1, a3); }
-    grid_barrier(f.bar_count, f.bar_gen);
-    stamp(f, nstamp);
-    ra.in = f.tA;
-    ra.xrho = f.x;
-    row_phase<L, RK_RSS>(ra, tw, xb);
-    grid_barrier(f.bar_count, f.bar_gen);
-    stamp(f, nstamp);
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)Q;
-         i += (long long)gridDim.x * blockDim.x) {
-      float s = 0.f;
-      for (int jj = 0; jj < J; ++jj) s += f.rss_all[jj * Q + i];
-      f.img[i] = cscale(f.rho_omega[i], sqrtf(s));
-    }
-  }
-}
-
-template <int L>
-static cudaError_t launch_frame_l(const FrameArgs& f, cudaStream_t s) {
-  if constexpr (!FrameGeo<L>::kOk) {
-    return cudaErrorNotSupported;
-  } else {
-  auto kern = frame_kernel<L>;
-  const size_t smem = FrameGeo<L>::SMEM;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int dev = 0, nsm = 0, per = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, FrameGeo<L>::NT, smem);
-  if (e != cudaSuccess) return e;
-  if (per < 1) return cudaErrorInvalidConfiguration;
-  int grid = nsm * (per > 2 ? 2 : per);
-  if (grid > kMaxFrameBlocks) grid = kMaxFrameBlocks;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(FrameGeo<L>::NT);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, f);
-  }
-}
-
 // ------------------------------------------------------------------ dispatch
 template <typename... KArgs, typename... Act>
 static cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
@@ -2036,15 +1237,11 @@ static cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (access_window(&attr[1].val.accessPolicyWindow)) {
-    attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
-    cfg.numAttrs = 2;
-  }
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
 }
 
@@ -2059,34 +1256,17 @@ static cudaError_t launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, si
   // cooperative (grid barriers); optionally with programmatic dependent launch, so the pass is
   // scheduled while the previous one drains (its CTAs reach a grid barrier only after
   // griddepcontrol.wait, i.e. after the previous pass has released every SM)
-  cudaLaunchAttribute attr[3];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = (pdl && pdl_enabled()) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  if (access_window(&attr[2].val.accessPolicyWindow)) {
-    attr[2].id = cudaLaunchAttributeAccessPolicyWindow;
-    cfg.numAttrs = 3;
-  }
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
 }
 
-// can the K5 pass run as one co-resident (cooperative) wave with the fused r update?
-template <int L>
-static bool col_fusable_l(int J) {
-  auto kern = col_kernel<L, CK_FFT_W_NORMAL>;
-  const size_t smem = ColGeo<L>::SMEM;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return false;
-  int dev = 0, nsm = 0, per = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, ColGeo<L>::THREADS, smem) != cudaSuccess) return false;
-  return (long long)(L / ColGeo<L>::CW) * J <= (long long)per * nsm;
-}
-
-// ... and the single-barrier k5cg_kernel (larger shared memory: the prefetch tile)
+// can the fused K5 + CG + K1 pass (k5cg_kernel) run as one co-resident (cooperative) wave?
 template <int L>
 static bool k5cg_fusable_l(int J) {
   if (ColGeo<L>::THREADS < 64) return false;
@@ -2116,10 +1296,7 @@ static cudaError_t launch_col_t(const ColArgs& a, const float2* tw, cudaStream_t
   const size_t smem = ColGeo<L>::SMEM;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int gy = ((MODE == CK_IFFT_W_CG || MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ) &&
-                  !a.rho_spread) ? a.J + 1 : a.J;
-  dim3 grid(L / ColGeo<L>::CW, gy);
-  if (MODE == CK_FFT_W_NORMAL && a.fuse_update) return launch_coop(kern, grid, dim3(ColGeo<L>::THREADS), smem, s, false, a, tw);
+  dim3 grid(L / ColGeo<L>::CW, a.J);
   return launch_k(kern, grid, dim3(ColGeo<L>::THREADS), smem, s, a, tw);
 }
 
@@ -2272,9 +1449,6 @@ static cudaError_t launch_fft2d_l(const float2* in, float2* out, int batch, int 
   cudaError_t launch_fft2d_##L(const float2* in, float2* out, int batch, int inverse, const float2* tw, \
                                cudaStream_t s);                                                 \
   int col_tiles_##L();                                                                          \
-  cudaError_t launch_frame_##L(const FrameArgs& f, cudaStream_t s);                             \
-  bool frame_ok_##L();                                                                          \
-  bool col_fusable_##L(int J);                                                                  \
   bool k5cg_fusable_##L(int J);
 #define NLV_INSTANTIATE(L)                                                                       \
   cudaError_t launch_col_##L(int mode, const ColArgs& a, const float2* tw, cudaStream_t s) {    \
@@ -2288,9 +1462,6 @@ static cudaError_t launch_fft2d_l(const float2* in, float2* out, int batch, int 
     return launch_fft2d_l<L>(in, out, batch, inverse, tw, s);                                    \
   }                                                                                              \
   int col_tiles_##L() { return L / ColGeo<L>::CW; }                                             \
-  cudaError_t launch_frame_##L(const FrameArgs& f, cudaStream_t s) { return launch_frame_l<L>(f, s); } \
-  bool frame_ok_##L() { return FrameGeo<L>::kOk; }                                              \
-  bool col_fusable_##L(int J) { return col_fusable_l<L>(J); }                                   \
   bool k5cg_fusable_##L(int J) { return k5cg_fusable_l<L>(J); }
 
 #define NLV_FOR_EACH_NG(X) X(16) X(32) X(48) X(64) X(96) X(128) X(192) X(256) X(384) X(512) X(768) X(1024)

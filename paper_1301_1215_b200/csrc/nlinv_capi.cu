@@ -60,24 +60,13 @@ struct nlinv_plan_s {
   float2 *tA = nullptr, *tB = nullptr, *c_omega = nullptr, *rho_omega = nullptr;
   float2 *S_all = nullptr, *S = nullptr, *S_sum = nullptr;   // per-coil terms; local sum; rank sum
   float *rss_all = nullptr, *rss = nullptr, *rss_sum = nullptr;
-  double* fred = nullptr;        // frame-kernel reduction partials
-  unsigned* fdone = nullptr;     // dataflow counters: [5][J + 1] completions + [2] queue heads
-  double* ftred = nullptr;       // dataflow per-task partials
-  bool dataflow = true;
-  unsigned* fbar = nullptr;      // frame-kernel grid barrier (count, generation)
-  bool use_frame = false;
-  bool gexec_valid_reset = false;
   int trace_mode = -1;                    // debug: column mode whose CTA timelines are recorded
-  bool rho_spread = true;                 // rho block in stripes over the coil tiles (NLINV_RHO_SPREAD=0: own CTAs)
   bool multi = false;                     // collective code path (world > 1 or NLINV_FORCE_NCCL=1)
-  bool fuse_k5 = false;                   // K5 + r update as one cooperative pass (world == 1, fits one wave)
-  bool fuse_k1 = false;                   // ... also K1 of the next iteration / the Newton update
-  bool k5cg1 = false;                     // fused K5 + CG + K1 with a single grid barrier (k5cg_kernel)
+  bool fused = false;                     // fused K5 + CG + K1 pass, one grid barrier (k5cg_kernel, R19)
   bool cg1 = false;                       // unfused CG: one (grouped) scalar all-reduce per iteration (R19)
   unsigned* kbar = nullptr;               // its grid barrier
-  double* kpart = nullptr;                // its <p, Ap> partials
+  double* kpart = nullptr;                // its dot partials
   unsigned long long* trace = nullptr;
-  unsigned long long* tstamp = nullptr;   // frame-kernel phase timestamps (nlinv_plan_phase_times)
   double *scal = nullptr, *partials = nullptr;
   unsigned* counter = nullptr;
   // host e2e staging (device side)
@@ -95,18 +84,12 @@ struct nlinv_plan_s {
   const float* pw_active = nullptr;    // real-valued P_k of the current frame (nullptr = binary P_k)
   float* pw_buf = nullptr;             // fixed device copy of the frame's sqrt(PSF) (graph-stable pointer)
   float2* h_raw = nullptr;   // staging of host raw samples (nlinv_stream_frame_radial)
-  void* slab = nullptr;      // one allocation for the per-iteration working set (L2 access window)
+  void* slab = nullptr;      // one allocation for the per-iteration working set
   long long mnnz_host = -1;  // count of midx; -1 = index list stale (P_k changed)
   // graph cache
   GraphKey gkey;
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t gstream = nullptr;          // graph stream for callers on the legacy default stream
-  // fused CG with the dx update on a side stream (dx_side_kernel overlapped with K2-K4):
-  // ping-pong direction buffers p / p2, fork/join events
-  bool dx_side = false;
-  float2* p2 = nullptr;
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t gev_in = nullptr, gev_out = nullptr;
   long long gkernels = 0;
   cudaStream_t last_stream = nullptr;
@@ -471,14 +454,13 @@ static void plan_free(nlinv_plan pl) {
   for (float* p : pl->tr_pw) cudaFree(p);
   cudaFree(pl->h_raw);
   cudaFree(pl->pw_buf);
-  if (pl->slab) {   // tA, tB, dx, r, p, c_omega live in the L2-persisting slab
-    clear_access_window(pl->slab);
+  if (pl->slab) {   // tA, tB, dx, r, p, c_omega live in one slab
     cudaFree(pl->slab);
     pl->tA = pl->tB = pl->dx = pl->r = pl->p = pl->c_omega = nullptr;
   }
   void* ptrs[] = {pl->tw, pl->winv, pl->mask, pl->xref, pl->dx, pl->r, pl->p, pl->Ap, pl->tA, pl->tB,
                   pl->c_omega, pl->rho_omega, pl->S_all, pl->S, pl->S_sum, pl->rss_all, pl->rss, pl->rss_sum,
-                  pl->fred, pl->fbar, pl->fdone, pl->ftred, pl->tstamp, pl->kbar, pl->kpart, pl->scal, pl->partials,
+                  pl->kbar, pl->kpart, pl->scal, pl->partials,
                   pl->counter, pl->h_frame, pl->h_x, pl->h_img, pl->midx, pl->mcount, pl->mnnz, pl->h_samples};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -486,10 +468,6 @@ static void plan_free(nlinv_plan pl) {
   if (pl->gev_in) cudaEventDestroy(pl->gev_in);
   if (pl->gev_out) cudaEventDestroy(pl->gev_out);
   if (pl->gstream) cudaStreamDestroy(pl->gstream);
-  if (pl->ev_fork) cudaEventDestroy(pl->ev_fork);
-  if (pl->ev_join) cudaEventDestroy(pl->ev_join);
-  if (pl->side) cudaStreamDestroy(pl->side);
-  cudaFree(pl->p2);
   for (cudaEvent_t e : pl->ev_pool) cudaEventDestroy(e);
 #ifdef NLINV_WITH_NCCL
   if (pl->comm) ncclCommDestroy(pl->comm);
@@ -560,12 +538,9 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
   ok &= alloc((void**)&pl->mask, N);
   ok &= alloc((void**)&pl->xref, sizeof(float2) * N * nb);
   // The per-CG-iteration working set (T intermediates, c|Omega, r, p, dx: ~65 MB at C2) is one
-  // slab. NLINV_L2PERSIST=1 marks it L2-persisting (access-policy window on every launch); measured
-  // on B200 at C2 that is within noise (+0.6 %: the passes are not DRAM bound), so it is off by
-  // default and the bench's per-frame L2 flush really flushes everything.
+  // slab. (An L2-persisting access-policy window over it was measured within noise at C2, +0.6 %:
+  // the passes are not DRAM bound; not kept.)
   {
-    const char* lp = std::getenv("NLINV_L2PERSIST");
-    const bool persist = (lp && lp[0] == '1');
     const size_t b_t = sizeof(float2) * pl->H * pl->J, b_v = sizeof(float2) * N * nb, b_c = sizeof(float2) * pl->Q * pl->J;
     const size_t tot_b = 2 * b_t + 3 * b_v + b_c;
     if (alloc(&pl->slab, tot_b)) {
@@ -576,7 +551,6 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
       pl->p = (float2*)(b + 2 * b_t + b_v);
       pl->dx = (float2*)(b + 2 * b_t + 2 * b_v);
       pl->c_omega = (float2*)(b + 2 * b_t + 3 * b_v);
-      if (persist) set_access_window(pl->slab, tot_b);
     } else {
       ok &= alloc((void**)&pl->dx, b_v);
       ok &= alloc((void**)&pl->r, b_v);
@@ -596,49 +570,19 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
     ok &= alloc((void**)&pl->S_sum, sizeof(float2) * pl->Q);
     ok &= alloc((void**)&pl->rss_sum, sizeof(float) * pl->Q);
   }
-  // The persistent whole-frame kernel is opt-in (NLINV_FRAME=1): on B200 at C2 the CUDA-graph
-  // multi-kernel path is faster (the single kernel pays instruction-cache misses and spills).
   {
-    const char* rs = std::getenv("NLINV_RHO_SPREAD");
-    pl->rho_spread = !(rs && rs[0] == '0');
     // single-reduction unfused CG: default where a reduction is a collective (multi-GPU path); on
     // one GPU the r update is cheaper as its own pass (measured), NLINV_CG1=1 forces it there
     const char* c1 = std::getenv("NLINV_CG1");
     pl->cg1 = c1 ? (c1[0] == '1') : pl->multi;
+    // fused K5 + CG + K1 with one grid barrier (world == 1, the K5 grid fits one co-resident wave);
+    // NLINV_FUSE_K5=0 forces the unfused passes
     const char* fk = std::getenv("NLINV_FUSE_K5");
-    pl->fuse_k5 = pl->rho_spread && !pl->multi && !(fk && fk[0] == '0') && col_fusable(nx, pl->J);
-    if (pl->fuse_k5) {
-      ok &= alloc((void**)&pl->kbar, sizeof(unsigned) * 4);   // [count, gen] + k5cg flip word
+    pl->fused = !pl->multi && !(fk && fk[0] == '0') && k5cg_fusable(nx, pl->J);
+    if (pl->fused) {
+      ok &= alloc((void**)&pl->kbar, sizeof(unsigned) * 4);
       ok &= alloc((void**)&pl->kpart, sizeof(double) * 8 * kMaxRedBlocks);
-      const char* f1 = std::getenv("NLINV_FUSE_K1");
-      pl->fuse_k1 = !(f1 && f1[0] == '0');
-      // one grid barrier per CG iteration (k5cg_kernel, R19) unless NLINV_K5CG1=0
-      const char* g1 = std::getenv("NLINV_K5CG1");
-      pl->k5cg1 = pl->fuse_k1 && !(g1 && g1[0] == '0') && k5cg_fusable(nx, pl->J);
-      // dx += gamma p off the critical path on a side stream (NLINV_DX_SIDE=1). Measured on B200 at
-      // C2 it is slower (223 vs 250 fps): the fused pass does not get shorter without its dx traffic
-      // and the side kernel slows K2-K4, so the update stays inside the fused pass by default.
-      const char* ds = std::getenv("NLINV_DX_SIDE");
-      pl->dx_side = pl->k5cg1 && (ds && ds[0] == '1');
-      if (pl->dx_side) {
-        ok &= alloc((void**)&pl->p2, sizeof(float2) * N * nb);
-        ok &= cudaStreamCreateWithFlags(&pl->side, cudaStreamNonBlocking) == cudaSuccess;
-        ok &= cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming) == cudaSuccess;
-        ok &= cudaEventCreateWithFlags(&pl->ev_join, cudaEventDisableTiming) == cudaSuccess;
-      }
     }
-  }
-  {
-    const char* fe = std::getenv("NLINV_FRAME");
-    pl->use_frame = !pl->multi && frame_supported(nx) && fe != nullptr && fe[0] == '1';
-  }
-  if (pl->use_frame) {
-    ok &= alloc((void**)&pl->fred, sizeof(double) * 3 * 6 * kMaxFrameBlocks);
-    ok &= alloc((void**)&pl->fbar, sizeof(unsigned) * 2);
-    ok &= alloc((void**)&pl->fdone, sizeof(unsigned) * (5 * (pl->J + 1) + 2));
-    ok &= alloc((void**)&pl->ftred, sizeof(double) * 6 * (size_t)col_tiles(nx) * (pl->J + 4));
-    const char* df = std::getenv("NLINV_DATAFLOW");
-    pl->dataflow = !(df && df[0] == '0');
   }
   ok &= alloc((void**)&pl->scal, sizeof(double) * SC_TOTAL);
   ok &= alloc((void**)&pl->partials, sizeof(double) * 8 * kMaxRedBlocks);
@@ -669,7 +613,6 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
   if (e == cudaSuccess) e = cudaMemcpy(pl->mask, m8.data(), N, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(pl->scal, 0, sizeof(double) * SC_TOTAL);
   if (e == cudaSuccess) e = cudaMemset(pl->counter, 0, sizeof(unsigned) * 4);
-  if (e == cudaSuccess && pl->fbar) e = cudaMemset(pl->fbar, 0, sizeof(unsigned) * 2);
   if (e == cudaSuccess && pl->kbar) e = cudaMemset(pl->kbar, 0, sizeof(unsigned) * 4);
   if (e != cudaSuccess) {
     std::string msg = std::string("plan upload: ") + cudaGetErrorString(e);
@@ -761,9 +704,8 @@ struct Enq {
   }
   nlinv_status col(int mode, ColArgs a) {
     // the fused K5 + CG pass is traced at CG iteration 1 only (a steady-state K5 -> CG -> K1 launch)
-    const bool fused = (mode == CK_FFT_W_NORMAL && a.fuse_update) || mode == CK_K5CG;
+    const bool fused = mode == CK_K5CG;
     a.trace = (pl->trace_mode == mode && (!fused || (a.iter == 1 && a.fuse_k1))) ? pl->trace : nullptr;
-    a.rho_spread = pl->rho_spread ? 1 : 0;
     a.winv = pl->winv;
     a.mask = pl->mask;
     a.pw = pl->pw_active;
@@ -772,8 +714,6 @@ struct Enq {
     a.counter = pl->counter;
     a.J = pl->J;
     const char* name = kColNames[mode];
-    if (mode == CK_FFT_W_NORMAL && a.fuse_update)
-      name = a.fuse_k1 ? "col_k5_cg_k1" : (a.fuse_newton ? "col_k5_newton" : "col_fft_w_normal_upd");
     if (mode == CK_FFT_W_RHS && a.fuse_k1) name = "col_rhs_k1";
     if (mode == CK_K5CG) name = a.fuse_k1 ? "col_k5_cg_k1" : "col_k5_newton";
     return kern(name, [&] { return launch_col(pl->ng, mode, a, pl->tw, s); });
@@ -783,31 +723,6 @@ struct Enq {
     a.c_omega = pl->c_omega;
     a.rho_omega = pl->rho_omega;
     return kern(kRowNames[mode], [&] { return launch_row(pl->ng, mode, a, pl->tw, s); });
-  }
-  // fork a kernel onto the plan's side stream (after everything enqueued so far on s) / join it
-  template <class F>
-  nlinv_status fork_side(const char* name, F&& launch) {
-    if (cudaEventRecord(pl->ev_fork, s) != cudaSuccess || cudaStreamWaitEvent(pl->side, pl->ev_fork, 0) != cudaSuccess)
-      return fail(pl, NLINV_ERR_CUDA, "side-stream fork");
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (pl->prof) {
-      e0 = pl->event();
-      cudaEventRecord(e0, pl->side);
-    }
-    cudaError_t e = launch(pl->side);
-    if (pl->prof) {
-      e1 = pl->event();
-      cudaEventRecord(e1, pl->side);
-      pl->prof_rec.push_back({name, e0, e1});
-    }
-    ++kernels;
-    if (e != cudaSuccess) return fail(pl, NLINV_ERR_CUDA, std::string(name) + ": " + cudaGetErrorString(e));
-    if (cudaEventRecord(pl->ev_join, pl->side) != cudaSuccess) return fail(pl, NLINV_ERR_CUDA, "side-stream record");
-    return NLINV_OK;
-  }
-  nlinv_status join_side() {
-    if (cudaStreamWaitEvent(s, pl->ev_join, 0) != cudaSuccess) return fail(pl, NLINV_ERR_CUDA, "side-stream join");
-    return NLINV_OK;
   }
   VecArgs vec() const {
     VecArgs v{};
@@ -888,7 +803,7 @@ nlinv_status enq_derivative_head(Enq& q, const float2* dx, bool cg_fused, int it
     ca.rho_p = pl->p;
     ca.rho_dx = pl->dx;
     ca.iter = iter;
-    if (pl->cg1 && !pl->fuse_k5) {   // r -= gamma A p of the previous iteration happens here (R19)
+    if (pl->cg1) {   // r -= gamma A p of the previous iteration happens here (R19)
       ca.cg1 = 1;
       ca.src2 = pl->Ap + pl->N;
       ca.rho_a = pl->Ap;
@@ -955,21 +870,11 @@ nlinv_status enq_normal(Enq& q, float alpha, const float2* dx, float2* out, bool
   cb.out_slot = SC_PAP_CHAT + iter;
   cb.out_slot_rho = SC_PAP_RHO + iter;
   cb.iter = iter;
-  const bool cg1 = cg && pl->cg1 && !pl->fuse_k5;
+  const bool cg1 = cg && pl->cg1;
   if (cg1) {   // also <r,Ap>, <Ap,Ap>, <r,r> for the single reduction (R19)
     cb.cg1 = 1;
     cb.r = pl->r + pl->N;
     cb.rho_r = pl->r;
-  }
-  if (cg && pl->fuse_k5) {
-    cb.fuse_update = 1;
-    cb.last_iter = (iter == last_iter) ? 1 : 0;
-    cb.r = pl->r + pl->N;
-    cb.rho_r = pl->r;
-    cb.bar_count = pl->kbar;
-    cb.bar_gen = pl->kbar + 1;
-    cb.fpart = pl->kpart;
-    cb.iter = iter;
   }
   TRY(q.col(CK_FFT_W_NORMAL, cb));
   if (cg1) {   // ONE grouped all-reduce of the four chat parts (the rho parts are replicated)
@@ -994,44 +899,6 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
   } else {
     TRY(q.kern("init_x", [&] { return launch_init_x(pl->xref, (long long)N, (long long)tot, q.s); }));
     TRY(q.kern("init_x", [&] { return launch_init_x(x, (long long)N, (long long)tot, q.s); }));
-  }
-  if (pl->use_frame && K > 0 && !pl->pw_active) {   // the frame kernel knows only the binary P_k
-    // one cooperative launch for the whole frame (all Newton steps, CG iterations, output)
-    FrameArgs f{};
-    f.x = x;
-    f.xref = pl->xref;
-    f.dx = pl->dx;
-    f.r = pl->r;
-    f.p = pl->p;
-    f.Ap = pl->Ap;
-    f.tA = pl->tA;
-    f.tB = pl->tB;
-    f.c_omega = pl->c_omega;
-    f.rho_omega = pl->rho_omega;
-    f.S_all = pl->S;
-    f.rss_all = pl->rss_all;
-    f.img = img;
-    f.y = frame;
-    f.winv = pl->winv;
-    f.mask = pl->mask;
-    f.tw = pl->tw;
-    f.scal = pl->scal;
-    f.red = pl->fred;
-    f.bar_count = pl->fbar;
-    f.bar_gen = pl->fbar + 1;
-    f.J = pl->J;
-    f.K = K;
-    f.L = L;
-    f.alpha0 = pl->prm.alpha0;
-    f.q = pl->prm.q;
-    f.dataflow = pl->dataflow ? 1 : 0;
-    f.done = pl->fdone;
-    f.qhead = pl->fdone + 5 * (pl->J + 1);
-    f.tred = pl->ftred;
-    f.S_coils = pl->S_all;
-    f.tstamp = pl->tstamp;
-    f.tstamp_cap = pl->tstamp ? 8192 : 0;
-    return q.kern("frame", [&] { return launch_frame(pl->ng, f, q.s); });
   }
   double alpha_d = pl->prm.alpha0;
   for (int nstep = 0; nstep < K; ++nstep, alpha_d *= pl->prm.q) {
@@ -1064,19 +931,17 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
     cb.rho_b = pl->xref;
     cb.rho_r = pl->r;
     cb.rho_p = pl->p;
-    if (pl->fuse_k1) {  // K1 of CG iteration 0 (p_0 = b) folded into the rhs pass
+    if (pl->fused) {  // K1 of CG iteration 0 (p_0 = b) folded into the rhs pass
       cb.fuse_k1 = 1;
       cb.t1 = pl->tA;
     }
     TRY(q.col(CK_FFT_W_RHS, cb));
     TRY(q.allreduce_scalar(SC_RR_CHAT + 0));
-    if (pl->fuse_k1) {
+    if (pl->fused) {
       // CG, fused form: per iteration K2, K3, K4 and one cooperative pass that does K5,
       // gamma, r -= gamma Ap, <r,r>, beta and K1 of the next iteration (or the Newton update)
-      float2* P[2] = {pl->p, pl->dx_side ? pl->p2 : pl->p};   // p_it lives in P[it % 2]
+      float2* pc = pl->p;
       for (int it = 0; it < L; ++it) {
-        float2* pc = P[it % 2];
-        float2* pn = P[(it + 1) % 2];
         RowArgs ra{};
         ra.in = pl->tA;
         ra.out = pl->tB;
@@ -1098,41 +963,28 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
         c5.partials = pl->partials;
         c5.out_slot = SC_PAP_CHAT + it;
         c5.out_slot_rho = SC_PAP_RHO + it;
-        c5.fuse_update = 1;
         c5.last_iter = (it == L - 1) ? 1 : 0;
         c5.fuse_k1 = (it < L - 1) ? 1 : 0;
-        c5.fuse_newton = (it == L - 1) ? 1 : 0;
         c5.iter = it;
         c5.r = pl->r + N;
         c5.rho_r = pl->r;
         c5.p = pc + N;
-        c5.rho_p = pn;
-        c5.p_out = pn + N;
-        c5.dx_side = pl->dx_side ? 1 : 0;
+        c5.rho_p = pc;
         c5.dx = pl->dx + N;
         c5.rho_dx = pl->dx;
         c5.t1 = pl->tA;
         c5.xc = x + N;
         c5.x_rho = x;
         c5.bar_count = pl->kbar;
-        c5.bar_gen = pl->kbar + 1;
         c5.fpart = pl->kpart;
-        if (pl->dx_side && it > 0) TRY(q.join_side());   // dx_side(it - 1) read p_{it-1} = P[(it+1) % 2]
-        TRY(q.col(pl->k5cg1 ? CK_K5CG : CK_FFT_W_NORMAL, c5));
-        if (pl->dx_side && it < L - 1) {                  // dx += gamma_it p_it, overlapped with K2-K4
-          VecArgs vd = q.vec();
-          vd.dx = pl->dx;
-          vd.p = pc;
-          vd.iter = it;
-          TRY(q.fork_side("dx_side", [&](cudaStream_t ss) { return launch_dx_side(vd, ss); }));
-        }
+        TRY(q.col(CK_K5CG, c5));
       }
       continue;
     }
     // CG: L iterations of the normal operator + vector updates
     for (int it = 0; it < L; ++it) {
       TRY(enq_normal(q, alpha, pl->p, pl->Ap, true, it, L - 1));
-      if (it < L - 1 && !pl->fuse_k5 && !pl->cg1) {  // r -= gamma Ap, <r, r> (dx is updated inside the next K1)
+      if (it < L - 1 && !pl->cg1) {  // r -= gamma Ap, <r, r> (dx is updated inside the next K1)
         VecArgs vr = q.vec();
         vr.r = pl->r;
         vr.Ap = pl->Ap;
@@ -1303,11 +1155,6 @@ static nlinv_status reconstruct_on(nlinv_plan pl, const nlinv_c32* frame, const 
   key.stream = s;
   key.pw = pl->pw_active;
   const bool use_graph = (s != nullptr) && !pl->prof && (std::getenv("NLINV_NO_GRAPH") == nullptr);
-  if (pl->gexec_valid_reset && pl->gexec) {
-    cudaGraphExecDestroy(pl->gexec);
-    pl->gexec = nullptr;
-    pl->gexec_valid_reset = false;
-  }
   if (use_graph && pl->gexec && pl->gkey == key) {
     CU(cudaGraphLaunch(pl->gexec, s));
     pl->launches += pl->gkernels;
@@ -1462,26 +1309,6 @@ extern "C" nlinv_status nlinv_plan_profile_json(nlinv_plan pl, char* buf, size_t
   pl->ev_used = 0;
   if (out.size() + 1 > len) return fail(pl, NLINV_ERR_SIZE, "profile buffer too small");
   std::memcpy(buf, out.c_str(), out.size() + 1);
-  return NLINV_OK;
-}
-
-// ------------------------------------------------------------------ frame-kernel phase timestamps
-extern "C" nlinv_status nlinv_plan_phase_times(nlinv_plan pl, int enable, unsigned long long* out, int cap,
-                                               int* count) {
-  if (!pl) return fail(pl, NLINV_ERR_ARG, "NULL plan");
-  if (enable) {
-    if (!pl->tstamp) CU(cudaMalloc((void**)&pl->tstamp, sizeof(unsigned long long) * 8192));
-    CU(cudaMemset(pl->tstamp, 0, sizeof(unsigned long long) * 8192));
-    pl->gexec_valid_reset = true;
-    return NLINV_OK;
-  }
-  if (!pl->tstamp || !out || !count) return fail(pl, NLINV_ERR_STATE, "phase timing not enabled");
-  CU(cudaDeviceSynchronize());
-  const int n = cap < 8192 ? cap : 8192;
-  CU(cudaMemcpy(out, pl->tstamp, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost));
-  int c = 0;
-  while (c < n && out[c] != 0) ++c;
-  *count = c;
   return NLINV_OK;
 }
 

@@ -29,37 +29,6 @@ int k4_planes(int ng, int J) {
   return J;
 }
 
-namespace {
-cudaAccessPolicyWindow g_apw{};
-bool g_apw_on = false;
-}  // namespace
-void set_access_window(void* base, size_t bytes) {
-  int dev = 0, maxp = 0, maxw = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
-  cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-  if (maxp <= 0 || maxw <= 0) return;
-  size_t win = bytes < (size_t)maxw ? bytes : (size_t)maxw;
-  size_t carve = win < (size_t)maxp ? win : (size_t)maxp;
-  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) != cudaSuccess) {
-    cudaGetLastError();
-    return;
-  }
-  g_apw.base_ptr = base;
-  g_apw.num_bytes = win;
-  g_apw.hitRatio = (float)((double)carve / (double)win);
-  g_apw.hitProp = cudaAccessPropertyPersisting;
-  g_apw.missProp = cudaAccessPropertyStreaming;
-  g_apw_on = true;
-}
-void clear_access_window(void* base) {
-  if (g_apw_on && g_apw.base_ptr == base) g_apw_on = false;
-}
-bool access_window(cudaAccessPolicyWindow* w) {
-  if (!g_apw_on) return false;
-  *w = g_apw;
-  return true;
-}
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("NLINV_PDL");
@@ -89,24 +58,6 @@ __global__ void __launch_bounds__(kVecThreads) newton_update_kernel(VecArgs a) {
     xv.x += fmaf(gamma, pv.x, d.x); xv.y += fmaf(gamma, pv.y, d.y);
     xv.z += fmaf(gamma, pv.z, d.z); xv.w += fmaf(gamma, pv.w, d.w);
     x4[i] = xv;
-  }
-}
-
-// dx += gamma_i p_i off the critical path (fused CG with dx_side): runs on a side stream, overlapped
-// with K2-K4 of the next iteration; p_i is the previous buffer of the ping-pong pair (the fused pass
-// wrote p_{i+1} into the other one). gamma_i from the same scalars, in the same order, as the pass.
-__global__ void __launch_bounds__(kVecThreads) dx_side_kernel(VecArgs a) {
-  pdl_wait();
-  pdl_trigger();
-  const float gamma = cg_gamma(a.scal, a.iter);
-  const bool hasdx = a.iter > 0;
-  const long long n2 = a.ntot / 2, stride = (long long)gridDim.x * blockDim.x;
-  const float4* p4 = reinterpret_cast<const float4*>(a.p);
-  float4* dx4 = reinterpret_cast<float4*>(a.dx);
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += stride) {
-    const float4 pv = p4[i];
-    const float4 d = hasdx ? dx4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-    dx4[i] = make_float4(fmaf(gamma, pv.x, d.x), fmaf(gamma, pv.y, d.y), fmaf(gamma, pv.z, d.z), fmaf(gamma, pv.w, d.w));
   }
 }
 
@@ -202,9 +153,6 @@ static int vec_grid(long long n) {
 
 cudaError_t launch_r_update(int /*ng*/, const VecArgs& a, cudaStream_t s) {
   return launch_k(r_update_kernel, dim3(vec_grid(a.ntot / 2)), dim3(kVecThreads), 0, s, a);
-}
-cudaError_t launch_dx_side(const VecArgs& a, cudaStream_t s) {
-  return launch_k(dx_side_kernel, dim3(vec_grid(a.ntot / 2)), dim3(kVecThreads), 0, s, a);
 }
 cudaError_t launch_newton_update(int /*ng*/, const VecArgs& a, cudaStream_t s) {
   return launch_k(newton_update_kernel, dim3(vec_grid(a.ntot / 2)), dim3(kVecThreads), 0, s, a);
@@ -350,30 +298,10 @@ cudaError_t launch_rss_sum(int ng, const float* rss_all, int J, float* rss, cuda
   const int Q = (ng / 2) * (ng / 2);
   return launch_k(rss_sum_kernel, dim3((Q + 255) / 256), dim3(256), 0, s, rss_all, J, rss, Q);
 }
-cudaError_t launch_frame(int ng, const FrameArgs& f, cudaStream_t s) {
-#define X(L) if (ng == L) return launch_frame_##L(f, s);
-  NLV_FOR_EACH_NG(X)
-#undef X
-  return cudaErrorInvalidValue;
-}
-bool col_fusable(int ng, int J) {
-#define X(L) if (ng == L) return col_fusable_##L(J);
-  NLV_FOR_EACH_NG(X)
-#undef X
-  return false;
-}
-
 bool k5cg_fusable(int ng, int J) {
 #define X(L) if (ng == L) return k5cg_fusable_##L(J);
   NLV_FOR_EACH_NG(X)
 #undef X
   return false;
 }
-bool frame_supported(int ng) {
-#define X(L) if (ng == L) return frame_ok_##L();
-  NLV_FOR_EACH_NG(X)
-#undef X
-  return false;
-}
-
 }  // namespace nlv

@@ -76,20 +76,14 @@ struct ColArgs {
   const float2* rho_b;     // rho_ref for RHS
   float2* rho_out;         // rho-slice output (Ap_rho / adjoint rho)
   unsigned long long* trace;  // debug timeline (-DNLV_TRACE builds only)
-  int rho_spread;          // 1: the rho block is processed in stripes by the coil tiles (no rho CTAs)
-  int fuse_update;         // K5: cooperative pass that also does r -= gamma A p and <r, r> (world == 1)
-  int last_iter;           // K5 fused: last CG iteration (no r update needed)
-  unsigned* bar_count;     // grid barrier of the fused K5
-  unsigned* bar_gen;
-  double* fpart;           // [6 * blocks] dot partials of the fused K5 passes
-  int fuse_k1;             // fused K5 / rhs: also run K1 of the next CG iteration (T1 into t1)
-  int fuse_newton;         // fused K5, last iteration: also x += dx + gamma p
-  float2* t1;              // K1 output (half image) for the fused variants
+  int last_iter;           // k5cg: last CG iteration (Newton update instead of the next K1)
+  unsigned* bar_count;     // k5cg: grid barrier word
+  double* fpart;           // k5cg: [8 * blocks] dot partials
+  int fuse_k1;             // k5cg / rhs: also run K1 of the next CG iteration (T1 into t1)
+  float2* t1;              // K1 output (half image) for the fused passes
   float2* xc;              // unknowns, chat blocks (fused Newton update)
   float2* x_rho;           // unknowns, rho block
   int iter;                // CG iteration (beta for CK_IFFT_W_CG)
-  float2* p_out;           // fused K5+CG+K1: p_{i+1} destination (ping-pong with p; nullptr = in place)
-  int dx_side;             // fused K5+CG+K1: dx += gamma p is left to dx_side_kernel on a side stream
   int cg1;                 // unfused single-reduction CG (R19): K5 also forms <r,Ap>, <Ap,Ap>, <r,r>;
                            // K1 applies r -= gamma Ap (A p from src2 / rho_a) before the p update
   float alpha;
@@ -109,31 +103,6 @@ struct RowArgs {
   int kchunk;              // K4 coils per CTA (set by the launcher)
 };
 int k4_planes(int ng, int J);  // number of K4 coil-sum planes
-
-// Persistent whole-frame kernel (world == 1): every buffer of the plan.
-constexpr int kMaxFrameBlocks = 1024;
-struct FrameArgs {
-  float2 *x, *xref, *dx, *r, *p, *Ap, *tA, *tB, *c_omega, *rho_omega, *S_all, *img;
-  float* rss_all;
-  const float2* y;
-  const float* winv;
-  const uint8_t* mask;
-  const float2* tw;
-  double* scal;
-  double* red;             // [3][2 * kMaxFrameBlocks] reduction partials
-  unsigned* bar_count;
-  unsigned* bar_gen;
-  int J, K, L;
-  double alpha0, q;
-  unsigned long long* tstamp;  // optional per-phase timestamps (ns), CTA 0
-  int tstamp_cap;
-  // dataflow CG segment
-  int dataflow;
-  unsigned* done;          // [5][J + 1] cumulative per-coil task completions
-  unsigned* qhead;         // [2] task-queue heads (alternating per CG iteration)
-  double* tred;            // [2 * ntile * (J + 4)] per-task <p, Ap> partials
-  float2* S_coils;         // [J][n][n] per-coil channel-sum terms
-};
 
 struct VecArgs {
   float2* x;         // unknowns (CG update of the last iteration adds into x)
@@ -165,23 +134,14 @@ cudaError_t launch_fft2d(int ng, const float2* in, float2* out, int batch, int i
                          float2* tmp, cudaStream_t s);
 bool supported_ng(int ng);
 bool pdl_enabled();
-// L2 access-policy window (persisting) attached to every launch of the library; set by the plan
-// that owns the working-set slab (the most recent one), cleared when it is freed
-void set_access_window(void* base, size_t bytes);
-void clear_access_window(void* base);
-bool access_window(cudaAccessPolicyWindow* w);      // programmatic dependent launch between passes (NLINV_PDL=0 disables)
 int col_tiles(int ng);  // column-kernel CTAs per coil
 cudaError_t launch_init_x(float2* x, long long nrho, long long ntot, cudaStream_t s);
-cudaError_t launch_frame(int ng, const FrameArgs& f, cudaStream_t s);
-bool frame_supported(int ng);
 cudaError_t launch_mask_compact(const uint8_t* mask, int N, int* counts, int* idx, int* nnz, cudaStream_t s);
 int mask_count_blocks(int N);
-cudaError_t launch_dx_side(const VecArgs& a, cudaStream_t s);
 cudaError_t launch_grid_radial(const float2* raw, int J, int nraw, const int* cells, const int* start, const int* sid,
                                const float* wgt, int nnz, size_t N, float2* y, cudaStream_t s);
 cudaError_t launch_scatter_samples(const float2* samples, const int* idx, const int* nnz, int nnz_cap, int J,
                                    size_t N, float2* y, cudaStream_t s);
-bool col_fusable(int ng, int J);
 bool k5cg_fusable(int ng, int J);
 cudaError_t launch_coil_sum(int ng, const float2* S_all, int J, float2* S, cudaStream_t s);
 cudaError_t launch_rss_sum(int ng, const float* rss_all, int J, float* rss, cudaStream_t s);

@@ -71,7 +71,6 @@ _SIGS = {
     "nlinv_mask_indices": (c_int, [c_void_p, c_void_p, c_int, ctypes.POINTER(c_int), c_void_p]),
     "nlinv_stream_frame_compact": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_int, c_int, c_void_p, c_void_p]),
     "nlinv_plan_set_profiling": (c_int, [c_void_p, c_int]),
-    "nlinv_plan_phase_times": (c_int, [c_void_p, c_int, c_void_p, c_int, ctypes.POINTER(c_int)]),
     "nlinv_plan_trace": (c_int, [c_void_p, c_int, c_void_p, c_int]),
     "nlinv_plan_profile_json": (c_int, [c_void_p, ctypes.c_char_p, ctypes.c_size_t]),
     "nlinv_plan_set_trajectory": (c_int, [c_void_p, c_int, c_int]),
@@ -358,16 +357,6 @@ class Plan:
         buf = ctypes.create_string_buffer(1 << 16)
         _check(_lib.nlinv_plan_profile_json(self._h, buf, len(buf)), self._h)
         return {k: {"launches": v[0], "ms": v[1]} for k, v in json.loads(buf.value.decode()).items()}
-
-    def phase_times_enable(self):
-        _check(_lib.nlinv_plan_phase_times(self._h, 1, None, 0, None), self._h)
-
-    def phase_times(self):
-        """Timestamps (ns) CTA 0 of the frame kernel took after each grid barrier."""
-        buf = (ctypes.c_ulonglong * 8192)()
-        cnt = c_int()
-        _check(_lib.nlinv_plan_phase_times(self._h, 0, buf, 8192, ctypes.byref(cnt)), self._h)
-        return [buf[i] for i in range(cnt.value)]
 
     def trace_enable(self, col_mode: int):
         _check(_lib.nlinv_plan_trace(self._h, int(col_mode), None, 0), self._h)

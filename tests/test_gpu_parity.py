@@ -322,16 +322,9 @@ def test_reconstruct_c2_full_frame():
 
 VARIANTS = {
     "fused (default, one grid barrier per CG iteration)": {},
-    "fused, dx update on a side stream (ping-pong p)": {"NLINV_DX_SIDE": "1"},
-    "fused, two grid barriers": {"NLINV_K5CG1": "0"},
-    "unfused K1/K5, textbook two reductions": {"NLINV_FUSE_K1": "0", "NLINV_FUSE_K5": "0"},
-    "unfused K1/K5, single reduction": {"NLINV_FUSE_K1": "0", "NLINV_FUSE_K5": "0", "NLINV_CG1": "1"},
-    "K5+update only": {"NLINV_FUSE_K1": "0"},
-    "rho in own CTAs": {"NLINV_RHO_SPREAD": "0"},
+    "unfused K1/K5, textbook two reductions": {"NLINV_FUSE_K5": "0"},
+    "unfused K1/K5, single reduction": {"NLINV_FUSE_K5": "0", "NLINV_CG1": "1"},
     "multi-GPU code path (single reduction), one-rank NCCL communicator": {"NLINV_FORCE_NCCL": "1"},
-    "multi-GPU code path, two reductions, one-rank NCCL": {"NLINV_FORCE_NCCL": "1", "NLINV_CG1": "0"},
-    "persistent frame kernel": {"NLINV_FRAME": "1", "NLINV_DATAFLOW": "0"},
-    "frame kernel, dataflow": {"NLINV_FRAME": "1", "NLINV_DATAFLOW": "1"},
 }
 
 
