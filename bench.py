@@ -56,10 +56,7 @@ def algo_bytes(name: str, ng: int, Jl: int, L: int = CG) -> float:
         "col_psf": 8 * Jl * N + N,
         "row_k4": 10 * Jl * N + 4 * N,
         "col_fft_w_normal": 20 * Jl * N + 4 * N + 18 * N,   # + rho slice: S, p_rho in, Ap_rho out
-        # K5 fused with the CG residual update (cooperative): T4, p, w^-1, r in, r out per coil;
-        # rho stripe: S, p_rho in, Ap_rho out and back in, r_rho in and out
-        "col_fft_w_normal_upd": 32 * Jl * N + 4 * N + 50 * N,
-        # ... + beta and K1 of the next iteration on the same tile. Compulsory operands only, each
+        # K5 fused with the CG update and K1 of the next iteration on the same tile. Compulsory operands only, each
         # counted once per launch: per coil T4 (Omega rows) 4, p 8, r 8+8, dx 8+8, p out 8, T1 out 4;
         # w^-1 once; rho block: coil-sum plane 2, p 8, r 8+8, dx 8+8, p out 8 (the A p_rho round
         # trip and the second p read are implementation re-reads, not counted)
@@ -80,15 +77,6 @@ def algo_bytes(name: str, ng: int, Jl: int, L: int = CG) -> float:
         "init_x": 8 * N * (Jl + 1),
         "image": 2 * N + N + 2 * N,
     }
-    if name == "frame":
-        # the persistent whole-frame kernel (NLINV_FRAME=1): every pass of the multi-kernel path
-        newton = sum(algo_bytes(k, ng, Jl) for k in ("col_ifft_w", "row_setpoint_fwd", "col_resadj", "row_k4",
-                                                    "col_fft_w_rhs", "newton_update"))
-        cgp = sum(algo_bytes(k, ng, Jl) for k in ("col_ifft_w_cg", "row_k2", "col_psf", "row_k4",
-                                                 "col_fft_w_normal"))
-        upd = algo_bytes("r_update", ng, Jl) * (L - 1)
-        out = algo_bytes("col_ifft_w", ng, Jl) + algo_bytes("row_rss", ng, Jl) + algo_bytes("image", ng, Jl)
-        return NEWTON * (newton + L * cgp + upd) + out
     return float(t.get(name, 0.0))
 
 
@@ -215,9 +203,14 @@ def _run_ours(args):
     ms_steps = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(ms_steps)
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([total_ms] + ms_steps, dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = float(t[0].item())
+        ms_steps = [float(v) for v in t[1:].tolist()]   # per-frame latency: the slowest rank
+    lat = sorted(ms_steps)
+
+    def pct(q):
+        return lat[min(len(lat) - 1, int(round(q * (len(lat) - 1))))]
     fps = args.steps / (total_ms / 1e3)
 
     # end to end through the public streaming API, every step: the frame's RAW radial samples
@@ -277,13 +270,15 @@ def _run_ours(args):
     tname, tv = top
     tb = algo_bytes(tname, NG, plan.count) * tv["launches"]
     achieved = tb / (tv["ms"] / 1e3) / 1e9
-    traffic = None
+    traffic = ncu_ms = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             tr = json.load(fh)
         traffic = tr.get(tname, {}).get("dram_bytes_per_launch")
+        us = tr.get(tname, {}).get("avg_us_ncu")
+        ncu_ms = us / 1e3 if us else None
     except Exception:
-        traffic = None
+        traffic = ncu_ms = None
     frame_bytes = sum(algo_bytes(k, NG, plan.count) * v["launches"] for k, v in prof.items())
     kernels = {k: {"launches": v["launches"], "ms": round(v["ms"], 4),
                    "share": round(v["ms"] / frame_ms, 4),
@@ -308,6 +303,8 @@ def _run_ours(args):
             "e2e_compact": {"value": round(args.steps / e2c_s, 3), "unit": "frames/s", "h2d_bytes_per_step": h2d_c,
                             "d2h_bytes_per_step": d2h,
                             "api": "nlinv_stream_frame_compact (pinned host gridded samples at P_k + mask in, image out)"},
+            "latency_ms": {"p50": round(pct(0.5), 4), "p95": round(pct(0.95), 4), "max": round(lat[-1], 4),
+                           "what": "device time of one frame (CUDA events around reconstruct), max over ranks"},
             "gpu_launches": launches,
             "clocks": clk,
             "roofline": {"bound": "hbm", "kernel": tname, "achieved": round(achieved, 1), "peak": peak,
@@ -315,6 +312,8 @@ def _run_ours(args):
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": tb / tv["launches"],
                          "avg_launch_ms": tv["ms"] / tv["launches"],
+                         "ncu_avg_launch_ms": ncu_ms,
+                         "frac_ncu": (round(tb / tv["launches"] / (ncu_ms / 1e3) / 1e9 / peak, 4) if ncu_ms else None),
                          "share_of_frame": round(tv["ms"] / frame_ms, 4),
                          "frame_algorithmic_GBps": round(frame_bytes / (frame_ms / 1e3) / 1e9, 1),
                          "method": "one extra frame with every kernel bracketed by CUDA events (no graph)",
@@ -324,42 +323,80 @@ def _run_ours(args):
     return out, world, rank
 
 
-def oracle_sample(cg_iters=CG):
-    """The fp64 oracle on a bounded sample of the workload: Newton step 0 (cg_iters CG) of frame 0."""
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def _oracle_inputs():
     import oracle as O
     import synth
     _, _, y = synth.frame_inputs(J, NG, t=0)
     y = y.astype(np.complex64).astype(np.complex128)
     P = O.radial_mask(NG, SPOKES, TURNS, 0).astype(np.float64)
-    winv, M = O.weights_inv(NG), O.fov_mask(NG)
-    x0 = O.initial_x(J, NG)
-    # one host core, as reported ("cores": 1): BLAS / OpenMP pools limited to a single thread
+    return O, y, P, O.weights_inv(NG), O.fov_mask(NG), O.initial_x(J, NG)
+
+
+def oracle_time(newton_steps, cores):
+    """The fp64 oracle (as it stands) on the C2 workload's frame 0: `newton_steps` IRGNM steps of
+    10 CG from the cold start, timed on `cores` host threads (cores > 1: the coil-parallel mode,
+    oracle.set_workers, bit-identical results). Returns seconds."""
+    O, y, P, winv, M, x0 = _oracle_inputs()
     from threadpoolctl import threadpool_limits
-    with threadpool_limits(limits=1):
-        t0 = time.perf_counter()
-        O.newton_step(x0, x0, y, P, winv, M, 1.0, cg_iters)
-        return time.perf_counter() - t0
+    O.set_workers(cores)
+    try:
+        with threadpool_limits(limits=1):
+            x = x0
+            t0 = time.perf_counter()
+            for n in range(newton_steps):
+                x, _ = O.newton_step(x, x0, y, P, winv, M, 1.0 * (1.0 / 3.0) ** n, CG)
+            return time.perf_counter() - t0
+    finally:
+        O.set_workers(1)
 
 
 def run_reference(args):
-    """--impl reference: the oracle as it stands, on the host cores, same metric/config."""
+    """--impl reference: the oracle as it stands on all host cores (coil-parallel mode), same metric
+    and workload. One step = one IRGNM Newton step (10 CG) of the C2 frame, i.e. 1/7 of a frame:
+    the frame rate is steps / 7 / time, and ms_per_step is the measured time of one such step."""
     world, rank, _ = _dist()
     if rank != 0:
         return None
+    cores = os.cpu_count() or 1
     for _ in range(args.warmup):
-        oracle_sample()
-    ts = [oracle_sample() for _ in range(args.steps)]
-    frame_s = NEWTON * statistics.mean(ts)   # each of the 7 Newton steps costs the same
-    fps = 1.0 / frame_s
-    sample = f"Newton step 0 of frame 0 (10 CG) of the C2 workload per step, frame time = 7 x mean step"
+        oracle_time(1, cores)
+    ts = [oracle_time(1, cores) for _ in range(args.steps)]
+    step_s = statistics.mean(ts)
+    fps = 1.0 / (NEWTON * step_s)
+    sample = (f"one Newton step (10 CG) of the C2 frame per step = 1/{NEWTON} frame; "
+              f"{args.steps} timed steps, mean {step_s:.3f} s, on {cores} threads ({_cpu_model()})")
     return {
         "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": frame_s * 1e3, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "ng": NG, "coils": J},
-        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "config": {"workload": WORKLOAD, "ng": NG, "coils": J, "step": f"1/{NEWTON} frame (one Newton step)"},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": sample,
+                         "cpu": _cpu_model()},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+
+
+def _relaunch(args):
+    """--gpus N > 1 without a torch.distributed launcher: re-exec this script under
+    torch.distributed.run with N ranks on this node (127.0.0.1)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -371,6 +408,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1:
+        sys.exit(_relaunch(args))
+    if world_env is not None and int(world_env) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}")
     if args.impl == "reference":
         out = run_reference(args)
         if out is not None:
@@ -379,11 +421,17 @@ def main():
     out, world, rank = run_ours(args)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
-            t = oracle_sample()
-            fps = 1.0 / (NEWTON * t)
-            out["cpu_baseline"] = {"value": round(fps, 6), "unit": "frames/s", "cores": 1, "kind": "oracle",
-                                   "sample": f"Newton step 0 of frame 0 (10 CG) at C2 took {t:.2f} s; "
-                                             f"frame = 7 such steps"}
+            # one whole C2 frame (7 Newton x 10 CG) of the oracle on all host cores (coil-parallel
+            # mode), and the same frame on one core
+            cores = os.cpu_count() or 1
+            t_all = oracle_time(NEWTON, cores)
+            t_one = oracle_time(NEWTON, 1) if cores > 1 else t_all
+            out["cpu_baseline"] = {"value": round(1.0 / t_all, 6), "unit": "frames/s", "cores": cores, "kind": "oracle",
+                                   "cpu": _cpu_model(),
+                                   "sample": f"one whole C2 frame (frame 0, 7 Newton x 10 CG, cold start) in "
+                                             f"{t_all:.2f} s on {cores} threads (coil-parallel mode)",
+                                   "single_core": {"value": round(1.0 / t_one, 6), "unit": "frames/s", "cores": 1,
+                                                   "sample": f"the same frame in {t_one:.2f} s on one core"}}
         print(json.dumps(out))
     if world > 1:
         import torch.distributed as dist

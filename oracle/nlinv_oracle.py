@@ -29,7 +29,7 @@ __all__ = [
     "OpCounters", "fc", "fch", "dft_matrix_1d", "fov_mask", "radial_mask", "radial_margin",
     "weights_inv", "coils_from_chat", "forward", "derivative", "adjoint", "normal",
     "inner", "cg", "irgnm", "image_from_x", "initial_x", "coil_partition", "Params",
-    "newton_step",
+    "newton_step", "set_workers",
 ]
 
 
@@ -52,6 +52,36 @@ COUNTERS = OpCounters()
 # --------------------------------------------------------------------------------------
 # Centred unitary DFT (reading A1: the paper only says "DTFT")
 # --------------------------------------------------------------------------------------
+# Coil-parallel timing mode (bench.py's all-core cpu_baseline, SURVEY §8(d) "coil-parallel mode over
+# all host cores"): set_workers(n) makes fc / fch transform the channels of a batch on n host threads,
+# one channel per task, each with the same library call as the serial path (numpy's FFT releases the
+# GIL). The per-channel transforms are independent, so results are bit-identical to the serial mode
+# (tests/test_oracle.py::test_workers_bit_identical); nothing else of the method changes.
+_POOL = None
+
+
+def set_workers(n: int) -> None:
+    global _POOL
+    from concurrent.futures import ThreadPoolExecutor
+    if _POOL is not None:
+        _POOL.shutdown()
+    _POOL = ThreadPoolExecutor(max_workers=n) if n > 1 else None
+
+
+def _per_channel(f, z: np.ndarray) -> np.ndarray:
+    if _POOL is None or z.ndim < 3 or z.shape[0] < 2:
+        return f(z)
+    return np.stack(list(_POOL.map(f, [z[j] for j in range(z.shape[0])])))
+
+
+def _fc1(z):
+    return np.fft.fftshift(np.fft.fft2(np.fft.ifftshift(z, axes=(-2, -1)), norm="ortho"), axes=(-2, -1))
+
+
+def _fch1(z):
+    return np.fft.fftshift(np.fft.ifft2(np.fft.ifftshift(z, axes=(-2, -1)), norm="ortho"), axes=(-2, -1))
+
+
 def fc(z: np.ndarray) -> np.ndarray:
     """Centred unitary 2D DFT over the last two axes (batched over leading axes = channels).
 
@@ -59,15 +89,13 @@ def fc(z: np.ndarray) -> np.ndarray:
     c = ng/2. Realised with the library FFT and index shifts (exact for even ng).
     """
     COUNTERS.fft += 1
-    return np.fft.fftshift(np.fft.fft2(np.fft.ifftshift(z, axes=(-2, -1)), norm="ortho"),
-                           axes=(-2, -1))
+    return _per_channel(_fc1, z)
 
 
 def fch(z: np.ndarray) -> np.ndarray:
     """Inverse (= adjoint) of ``fc``."""
     COUNTERS.fft += 1
-    return np.fft.fftshift(np.fft.ifft2(np.fft.ifftshift(z, axes=(-2, -1)), norm="ortho"),
-                           axes=(-2, -1))
+    return _per_channel(_fch1, z)
 
 
 def dft_matrix_1d(L: int, inverse: bool = False) -> np.ndarray:

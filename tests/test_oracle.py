@@ -425,3 +425,17 @@ def test_image_pins_catch_mutations(kind, monkeypatch):
         except AssertionError:
             caught += 1
     assert caught >= 1
+
+
+def test_workers_bit_identical():
+    # the coil-parallel timing mode (set_workers) runs the same per-channel library call on host
+    # threads: a Newton step must be bit-identical to the serial oracle
+    ng, J = 32, 4
+    x, _, y, P, winv, M = _problem(ng=ng, J=J, seed=5)
+    ref = O.newton_step(x, x, y, P, winv, M, 1.0, 4)
+    O.set_workers(4)
+    try:
+        par = O.newton_step(x, x, y, P, winv, M, 1.0, 4)
+    finally:
+        O.set_workers(1)
+    assert np.array_equal(ref[0], par[0]) and ref[1] == par[1]
