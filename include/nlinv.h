@@ -216,6 +216,11 @@ nlinv_status nlinv_plan_stats(nlinv_plan plan, nlinv_stats* out);
 nlinv_status nlinv_debug_fft2d(nlinv_plan plan, const nlinv_c32* in, nlinv_c32* out, int batch, int inverse,
                                void* stream);
 
+/* Debug: how many thread-block clusters of the cluster-fused K2 -> K3 -> K4 pass (one cluster per
+ * coil, DSMEM transposes) can be co-resident on the current device at grid size ng
+ * (cudaOccupancyMaxActiveClusters); < 0 if that pass is not built for ng. Needs a device. */
+int nlinv_debug_k234_clusters(int ng);
+
 /* Number of kernels this library enqueued since plan creation (launch-count evidence). */
 long long nlinv_plan_launch_count(nlinv_plan plan);
 

@@ -1228,6 +1228,218 @@ __global__ void __launch_bounds__(256, NLV_MINB) row_kernel(RowArgs a, const flo
   }
 }
 
+// ------------------------------------------------------------------ cluster-fused K2 -> K3 -> K4
+// One thread-block cluster per coil runs the three middle passes of the normal operator
+// without leaving the chip: CTA b of the C-CTA cluster owns R = 256/T Omega rows
+// (the row passes) and W = 2R grid columns (the column pass), and the two row<->column transposes
+// go through distributed shared memory (each CTA pulls its operand from the other CTAs' shared
+// memory with ld.shared::cluster after a cluster barrier) instead of T2/T3 round trips through L2
+// and two kernel boundaries. P:244 (per-channel FFTs + point-wise operations), P:339 (the FFT is the
+// most time-consuming operation).
+//   phase 1 (K2, rows):    T1 row -> row IFFT -> dc; z = M(p_rho c + rho dc)/L -> row FFT -> X (own, [R][L])
+//   cluster barrier; pull my W columns of all n Omega rows from the cluster's X into registers;
+//   cluster barrier (every X is free again)
+//   phase 2 (K3, columns): column FFT -> x P_k -> column IFFT (Omega rows) -> X (own, [n][W])
+//   cluster barrier
+//   phase 3 (K4, rows):    pull my R rows (all L columns) from the cluster's X -> row IFFT -> u;
+//                          S_j = conj(c_j) u (per-coil plane, summed in coil order by the consumer);
+//                          v = conj(rho) u / L -> row FFT -> T4 (global, read by the fused K5 pass)
+// Shared memory: twiddles, X (the exchanged data, R*L = n*W values) and D (the FFT exchange buffer),
+// ~101 KB at L = 384, i.e. two CTAs per SM so that J clusters of C CTAs are co-resident.
+template <int L>
+struct K234Geo {
+  static constexpr int T = Cfg<L>::T;
+  static constexpr int R = 256 / T;          // Omega rows per CTA (row phases: R groups of T threads)
+  static constexpr int C = ((L / 2) / R) > 0 ? (L / 2) / R : 1;   // CTAs per cluster (= per coil)
+  static constexpr int W = L / C;            // columns per CTA (column phase)
+  static constexpr int CW = ColGeo<L>::CW;   // columns per column round
+  static constexpr int ROUNDS = W / CW;
+  static constexpr bool kOk = (R * T == 256) && (C >= 2) && (C <= 16) && ((L / 2) % R == 0) && (L % C == 0) &&
+                              (W % CW == 0) && (ROUNDS == 2) && (CW * T == 256) && (Sched<L>::kSymmetric);
+  static constexpr size_t XN = (size_t)R * L;               // == (L/2) * W
+  static constexpr size_t SMEM = sizeof(float2) * ((size_t)L + 2 * XN);
+};
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
+// shared::cta address of this CTA's buffer -> shared::cluster address of the same buffer in CTA `rank`
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, uint32_t rank) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float2 ld_dsmem(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];\n" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+
+template <int L>
+__global__ void __launch_bounds__(256, 2) k234_kernel(RowArgs a, const float2* __restrict__ twg) {
+  using G = K234Geo<L>;
+  using C_ = Cfg<L>;
+  using S = Sched<L>;
+  constexpr int T = C_::T, E = C_::E, R = G::R, W = G::W, CW = G::CW;
+  constexpr int n = L / 2, q = L / 4;
+  constexpr size_t H = (size_t)n * L, Q = (size_t)n * n;
+  constexpr float invL = 1.0f / (float)L;
+  extern __shared__ float4 smem_raw[];
+  float2* tw = reinterpret_cast<float2*>(smem_raw);
+  float2* X = tw + L;          // exchanged data: phase 1 out [R][L], phase 2 out [n][W]
+  float2* D = X + G::XN;       // FFT exchange buffer
+  const int b = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
+  tw_copy_async(tw, twg, L);
+
+  // ---- operands fixed for the Newton step / the frame: read before griddepcontrol.wait
+  // phase-2 mask bits of this thread's two columns (k-space rows out_idx(t, e))
+  const int cc = tid % CW, ct = tid / CW;
+  uint32_t mb[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int x = W * b + CW * h + cc;
+    uint32_t m = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) m |= (__ldcg(a.mask + (size_t)S::out_idx(ct, e) * L + x) ? 1u : 0u) << e;
+    mb[h] = m;
+  }
+  const int g = tid / T, t = tid % T;
+  const int yy = R * b + g;      // Omega row of this group (phases 1 and 3)
+  pdl_wait();
+  pdl_trigger();
+
+  // ================= phase 1: K2 on row yy
+  {
+    RowBuf buf{D + (size_t)g * L};
+    float2 v[E];
+    const float2* src = a.in + (size_t)j * H + (size_t)yy * L;
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = src[S::in_idx(t, psh_in<L>(e))];
+    tw_wait();
+    fft<L, +1>(v, t, tw, buf, SyncWarp{});
+    float2 w[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) w[e] = v[psh_out<L>(e)];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (out_is_omega<L>(e)) {
+        const int k = S::out_idx(t, e);
+        const float2 cv = __ldcg(a.c_omega + (size_t)j * Q + (size_t)yy * n + (k - q));
+        const float2 rv = __ldcg(a.rho_omega + (size_t)yy * n + (k - q));
+        const float2 pr = a.prho[(size_t)(q + yy) * L + k];
+        v[e] = cscale(cadd(cmul(pr, cv), cmul(rv, w[e])), invL);
+      } else {
+        v[e] = make_float2(0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) w[e] = v[psh_in<L>(e)];
+    fft<L, -1, omega_shift_zmask<L>()>(w, t, tw, buf, SyncWarp{});
+    float2* xo = X + (size_t)g * L;
+#pragma unroll
+    for (int e = 0; e < E; ++e) xo[S::out_idx(t, e)] = w[psh_out<L>(e)];
+  }
+  cluster_sync_all();   // X of every CTA holds its R rows of the row-FFT'd z
+
+  // ================= pull: my W columns of all n Omega rows (column-FFT input pattern, both rounds)
+  float2 in2[2][E / 2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int x = W * b + CW * h + cc;
+    int u = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (in_is_omega<L>(e)) {
+        const int yr = S::in_idx(ct, e), r = yr - q;
+        const uint32_t ad = dsmem_addr(X + (size_t)(r % R) * L + x, (uint32_t)(r / R));
+        in2[h][u++] = cneg_if(ld_dsmem(ad), yr & 1);
+      }
+    }
+  }
+  cluster_sync_all();   // every CTA has its inputs: X is free
+  // round 1's inputs stay in registers; round 2's are parked in X at their own (row, column) slot of
+  // the [n][W] layout, the slot round 2 later overwrites with its output (after the transform's
+  // block barriers, i.e. after every parked value has been read back)
+  {
+    int u = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (in_is_omega<L>(e)) X[(size_t)(S::in_idx(ct, e) - q) * W + CW + cc] = in2[1][u++];
+  }
+
+  // ================= phase 2: K3 on columns W b + CW h + cc, two rounds
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    ColBuf<CW> buf{D, cc};
+    float2 v[E];
+    {
+      int u = 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if (in_is_omega<L>(e)) {
+          v[e] = (h == 0) ? in2[0][u] : X[(size_t)(S::in_idx(ct, e) - q) * W + CW + cc];
+          ++u;
+        } else {
+          v[e] = make_float2(0.f, 0.f);
+        }
+      }
+    }
+    fft<L, -1, omega_in_zmask<L>()>(v, ct, tw, buf, SyncBlock{});
+    const uint32_t mh = (h == 0) ? mb[0] : mb[1];
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = ((mh >> e) & 1u) ? v[e] : make_float2(0.f, 0.f);   // (-1)^k signs cancel
+    fft<L, +1>(v, ct, tw, buf, SyncBlock{});
+    const int xl = CW * h + cc;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (out_is_omega<L>(e)) {
+        const int k = S::out_idx(ct, e);
+        X[(size_t)(k - q) * W + xl] = cscale(v[e], invL * sgn_of(k));
+      }
+    }
+  }
+  cluster_sync_all();   // X of every CTA holds its W columns of the Omega rows
+
+  // ================= phase 3: K4 on row yy
+  {
+    RowBuf buf{D + (size_t)g * L};
+    float2 v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int x = S::in_idx(t, psh_in<L>(e));
+      v[e] = ld_dsmem(dsmem_addr(X + (size_t)yy * W + (x % W), (uint32_t)(x / W)));
+    }
+    cluster_arrive();    // this CTA's remote reads are done (waited for before exit)
+    fft<L, +1>(v, t, tw, buf, SyncWarp{});
+    float2 w[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) w[e] = v[psh_out<L>(e)];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (out_is_omega<L>(e)) {
+        const int k = S::out_idx(t, e);
+        const float2 cv = __ldcg(a.c_omega + (size_t)j * Q + (size_t)yy * n + (k - q));
+        const float2 rv = __ldcg(a.rho_omega + (size_t)yy * n + (k - q));
+        const float2 uu = w[e];
+        a.S[(size_t)j * Q + (size_t)yy * n + (k - q)] = cmulc(cv, uu);   // Table 1 "sum c_j" term of coil j
+        v[e] = cscale(cmulc(rv, uu), invL);
+      } else {
+        v[e] = make_float2(0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) w[e] = v[psh_in<L>(e)];
+    fft<L, -1, omega_shift_zmask<L>()>(w, t, tw, buf, SyncWarp{});
+    float2* dst = a.out + (size_t)j * H + (size_t)yy * L;
+#pragma unroll
+    for (int e = 0; e < E; ++e) dst[S::out_idx(t, e)] = w[psh_out<L>(e)];
+  }
+  cluster_wait();        // no CTA leaves while another may still read its X
+}
+
 // ------------------------------------------------------------------ dispatch
 template <typename... KArgs, typename... Act>
 static cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
@@ -1355,6 +1567,74 @@ static cudaError_t launch_row_l(int mode, const RowArgs& a, const float2* tw, cu
   return cudaErrorInvalidValue;
 }
 
+template <int L>
+static bool k234_ok_l() {
+  if constexpr (!K234Geo<L>::kOk) {
+    return false;
+  } else {
+    auto kern = k234_kernel<L>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K234Geo<L>::SMEM) != cudaSuccess)
+      return false;
+    if (K234Geo<L>::C > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+      return false;
+    return true;
+  }
+}
+
+template <int L>
+static int k234_max_clusters_l() {
+  if constexpr (!K234Geo<L>::kOk) {
+    return -1;
+  } else {
+    using G = K234Geo<L>;
+    auto kern = k234_kernel<L>;
+    if (!k234_ok_l<L>()) return -2;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(G::C, 64);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = G::SMEM;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = G::C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) return -3;
+    return n;
+  }
+}
+
+template <int L>
+static cudaError_t launch_k234_l(const RowArgs& a, const float2* tw, cudaStream_t s) {
+  if constexpr (!K234Geo<L>::kOk) {
+    return cudaErrorInvalidConfiguration;
+  } else {
+    using G = K234Geo<L>;
+    auto kern = k234_kernel<L>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    if (e != cudaSuccess) return e;
+    if (G::C > 8 && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
+      return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(G::C, a.J);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = G::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = G::C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, kern, a, tw);
+  }
+}
+
 // ------------------------------------------------------------------ plain batched 2D transform
 // (debug / micro-benchmark entry: centred unitary F_c or F_c^H of `batch` images)
 template <int L, int DIR>
@@ -1449,7 +1729,10 @@ static cudaError_t launch_fft2d_l(const float2* in, float2* out, int batch, int 
   cudaError_t launch_fft2d_##L(const float2* in, float2* out, int batch, int inverse, const float2* tw, \
                                cudaStream_t s);                                                 \
   int col_tiles_##L();                                                                          \
-  bool k5cg_fusable_##L(int J);
+  bool k5cg_fusable_##L(int J);                                                                  \
+  bool k234_ok_##L();                                                                            \
+  cudaError_t launch_k234_##L(const RowArgs& a, const float2* tw, cudaStream_t s);              \
+  int k234_max_clusters_##L();
 #define NLV_INSTANTIATE(L)                                                                       \
   cudaError_t launch_col_##L(int mode, const ColArgs& a, const float2* tw, cudaStream_t s) {    \
     return launch_col_l<L>(mode, a, tw, s);                                                      \
@@ -1462,7 +1745,10 @@ static cudaError_t launch_fft2d_l(const float2* in, float2* out, int batch, int 
     return launch_fft2d_l<L>(in, out, batch, inverse, tw, s);                                    \
   }                                                                                              \
   int col_tiles_##L() { return L / ColGeo<L>::CW; }                                             \
-  bool k5cg_fusable_##L(int J) { return k5cg_fusable_l<L>(J); }
+  bool k5cg_fusable_##L(int J) { return k5cg_fusable_l<L>(J); }                                  \
+  bool k234_ok_##L() { return k234_ok_l<L>(); }                                                  \
+  cudaError_t launch_k234_##L(const RowArgs& a, const float2* tw, cudaStream_t s) { return launch_k234_l<L>(a, tw, s); } \
+  int k234_max_clusters_##L() { return k234_max_clusters_l<L>(); }
 
 #define NLV_FOR_EACH_NG(X) X(16) X(32) X(48) X(64) X(96) X(128) X(192) X(256) X(384) X(512) X(768) X(1024)
 NLV_FOR_EACH_NG(NLV_DECLARE)

@@ -63,6 +63,7 @@ struct nlinv_plan_s {
   int trace_mode = -1;                    // debug: column mode whose CTA timelines are recorded
   bool multi = false;                     // collective code path (world > 1 or NLINV_FORCE_NCCL=1)
   bool fused = false;                     // fused K5 + CG + K1 pass, one grid barrier (k5cg_kernel, R19)
+  bool k234 = false;                      // cluster-fused K2 -> K3 -> K4 in the fused CG loop (k234_kernel)
   bool cg1 = false;                       // unfused CG: one (grouped) scalar all-reduce per iteration (R19)
   unsigned* kbar = nullptr;               // its grid barrier
   double* kpart = nullptr;                // its dot partials
@@ -579,6 +580,12 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
     // NLINV_FUSE_K5=0 forces the unfused passes
     const char* fk = std::getenv("NLINV_FUSE_K5");
     pl->fused = !pl->multi && !(fk && fk[0] == '0') && k5cg_fusable(nx, pl->J);
+    // cluster-fused K2 -> K3 -> K4 (DSMEM transposes) inside the fused CG loop: opt-in (NLINV_K234=1).
+    // Measured on B200 at C2 it is slower than the three PDL-chained passes (45.5 vs 40.4 us per
+    // iteration, eager events): with 12 coils x 12-CTA clusters on 148 SMs some SMs host two CTAs
+    // and every cluster barrier waits for them.
+    const char* kc = std::getenv("NLINV_K234");
+    pl->k234 = pl->fused && (kc && kc[0] == '1') && k234_supported(nx);
     if (pl->fused) {
       ok &= alloc((void**)&pl->kbar, sizeof(unsigned) * 4);
       ok &= alloc((void**)&pl->kpart, sizeof(double) * 8 * kMaxRedBlocks);
@@ -942,21 +949,36 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
       // gamma, r -= gamma Ap, <r,r>, beta and K1 of the next iteration (or the Newton update)
       float2* pc = pl->p;
       for (int it = 0; it < L; ++it) {
-        RowArgs ra{};
-        ra.in = pl->tA;
-        ra.out = pl->tB;
-        ra.prho = pc;
-        TRY(q.row(RK_K2, ra));
-        ColArgs c3{};
-        c3.in = pl->tB;
-        c3.out = pl->tA;
-        TRY(q.col(CK_PSF, c3));
-        TRY(enq_k4_allreduce(q));
         ColArgs c5{};
+        if (pl->k234) {   // K2 -> K3 -> K4, one cluster per coil: T1 (tA) -> T4 (tB) + per-coil S planes
+          RowArgs ra{};
+          ra.in = pl->tA;
+          ra.out = pl->tB;
+          ra.prho = pc;
+          ra.S = pl->S_all;
+          ra.mask = pl->mask;
+          ra.J = pl->J;
+          ra.c_omega = pl->c_omega;
+          ra.rho_omega = pl->rho_omega;
+          TRY(q.kern("k234", [&] { return launch_k234(pl->ng, ra, pl->tw, q.s); }));
+          c5.S = pl->S_all;
+          c5.nS = pl->J;
+        } else {
+          RowArgs ra{};
+          ra.in = pl->tA;
+          ra.out = pl->tB;
+          ra.prho = pc;
+          TRY(q.row(RK_K2, ra));
+          ColArgs c3{};
+          c3.in = pl->tB;
+          c3.out = pl->tA;
+          TRY(q.col(CK_PSF, c3));
+          TRY(enq_k4_allreduce(q));
+          set_S(pl, c5);
+        }
         c5.in = pl->tB;
         c5.src2 = pc + N;
         c5.out = pl->Ap + N;
-        set_S(pl, c5);
         c5.rho_a = pc;
         c5.rho_out = pl->Ap;
         c5.alpha = alpha;
@@ -1426,3 +1448,6 @@ extern "C" nlinv_status nlinv_stream_frame_radial(nlinv_plan pl, const nlinv_c32
   CU(cudaStreamSynchronize(s));
   return NLINV_OK;
 }
+
+// debug: co-resident clusters of the cluster-fused K2-K3-K4 kernel at grid size ng (< 0: not built)
+extern "C" int nlinv_debug_k234_clusters(int ng) { return k234_max_clusters(ng); }

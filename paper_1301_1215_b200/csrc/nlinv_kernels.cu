@@ -304,4 +304,24 @@ bool k5cg_fusable(int ng, int J) {
 #undef X
   return false;
 }
+bool k234_supported(int ng) {
+#define X(L) if (ng == L) return k234_ok_##L();
+  NLV_FOR_EACH_NG(X)
+#undef X
+  return false;
+}
+cudaError_t launch_k234(int ng, const RowArgs& a, const float2* tw, cudaStream_t s) {
+#define X(L) if (ng == L) return launch_k234_##L(a, tw, s);
+  NLV_FOR_EACH_NG(X)
+#undef X
+  return cudaErrorInvalidValue;
+}
+
+int k234_max_clusters(int ng) {
+#define X(L) if (ng == L) return k234_max_clusters_##L();
+  NLV_FOR_EACH_NG(X)
+#undef X
+  return -1;
+}
+
 }  // namespace nlv

@@ -99,6 +99,7 @@ struct RowArgs {
   const float2* prho;      // rho part of the direction, full grid (K2)
   float2* S;               // K4: coil-sum planes [chunks][n][n] (ordered within a chunk)
   float* rss;              // [J][n][n] per-coil |c_j|^2 (RSS)
+  const uint8_t* mask;     // [ng][ng] P_k (cluster-fused K2-K3-K4)
   int J;
   int kchunk;              // K4 coils per CTA (set by the launcher)
 };
@@ -143,6 +144,10 @@ cudaError_t launch_grid_radial(const float2* raw, int J, int nraw, const int* ce
 cudaError_t launch_scatter_samples(const float2* samples, const int* idx, const int* nnz, int nnz_cap, int J,
                                    size_t N, float2* y, cudaStream_t s);
 bool k5cg_fusable(int ng, int J);
+// cluster-fused K2 -> K3 -> K4 (one thread-block cluster per coil, DSMEM transposes)
+bool k234_supported(int ng);
+cudaError_t launch_k234(int ng, const RowArgs& a, const float2* tw, cudaStream_t s);
+int k234_max_clusters(int ng);
 cudaError_t launch_coil_sum(int ng, const float2* S_all, int J, float2* S, cudaStream_t s);
 cudaError_t launch_rss_sum(int ng, const float* rss_all, int J, float* rss, cudaStream_t s);
 

@@ -65,6 +65,7 @@ _SIGS = {
     "nlinv_reconstruct_host": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "nlinv_plan_stats": (c_int, [c_void_p, ctypes.POINTER(Stats)]),
     "nlinv_debug_fft2d": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]),
+    "nlinv_debug_k234_clusters": (c_int, [c_int]),
     "nlinv_plan_launch_count": (c_ll, [c_void_p]),
     "nlinv_stream_frame": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]),
     "nlinv_stream_reset": (c_int, [c_void_p]),

@@ -138,7 +138,10 @@ def test_divergence_flag():
     """The divergence guard (nlinv_plan_stats 'diverged': a residual > 10x the first one).
     A nearly unregularised Gauss-Newton step (alpha_0 = 1e-6) from a prior with tiny sensitivities
     overshoots on this bilinear model: the oracle's residual grows ~22x at Newton step 1, and the
-    GPU must report the same history and raise the flag."""
+    GPU must raise the flag. With alpha_0 = 1e-6 the CG system is so ill-conditioned that fp32
+    arithmetic alone moves the step-1 residual by ~7 % from the fp64 oracle (1468 vs 1584): the GPU
+    history is compared with the fp32 model of the oracle (_irgnm_fp32 below) at 1e-2 and with the
+    oracle's at the divergence level."""
     B = _B()
     ng, J, K, L = 32, 4, 3, 10
     _, _, y = synth.frame_inputs(J, ng)
@@ -155,7 +158,9 @@ def test_divergence_flag():
     _, hist = O.irgnm(y.astype(np.complex128), mask, P, P, K, L, O.Params(alpha0=1e-6))
     assert hist[1] > 10 * hist[0]                      # the oracle diverges here
     assert st["diverged"] == 1 and not st["cg_breakdown"]
-    assert abs(st["residual"][1] / hist[1] - 1) < 1e-2, (st["residual"], hist)
+    _, h32 = _irgnm_fp32(y.astype(np.complex128), mask, P, K, L, alpha0=1e-6)
+    assert np.allclose(st["residual"], h32, rtol=1e-2), (st["residual"], h32, hist)
+    assert abs(st["residual"][0] / hist[0] - 1) < 1e-5 and st["residual"][1] > 10 * st["residual"][0]
     # the same data from the regular start does not diverge
     plan2 = B.Plan(ng, J, mask)
     plan2.reconstruct(torch.from_numpy(y).cuda(), None, K, L)
@@ -187,11 +192,13 @@ def _irgnm_fp32(y, P, x0, K, L, alpha0=1.0, q=1.0 / 3.0):
     x = x0.astype(f32)
     xref = x.copy()
     y = y.astype(f32)
+    hist = []
     for n in range(K):
         alpha = np.float32(alpha0 * q ** n)
         rho, chat = x[0], x[1:]
         c = fch(winv * chat)
         r = P * y - P * fc(M * rho * c)
+        hist.append(float(np.linalg.norm(r.astype(np.complex128))))
         u = M * fch(P * r)
 
         def adj(u):
@@ -220,7 +227,7 @@ def _irgnm_fp32(y, P, x0, K, L, alpha0=1.0, q=1.0 / 3.0):
             p = rr_ + beta * p
             rr = rn
         x = x + dx
-    return x.astype(np.complex128)
+    return x.astype(np.complex128), hist
 
 
 @pytest.mark.parametrize("ng,J,S,T,K,L", [(32, 8, 8, 1, 2, 10),
@@ -242,7 +249,7 @@ def test_kb_frame_within_fp32_model_bound(ng, J, S, T, K, L):
     x0 = O.initial_x(J, ng)
     xo, _ = O.irgnm(yo, P, x0, x0, K, L)
     io = O.image_from_x(xo)
-    x32 = _irgnm_fp32(yo, P, x0, K, L)
+    x32, _ = _irgnm_fp32(yo, P, x0, K, L)
     e_model = rel(O.image_from_x(x32), io)
     _, img = plan.reconstruct(y, None, K, L)
     e_gpu = rel(host(img), io)

@@ -1,0 +1,8 @@
+#!/bin/bash
+# Quick GPU iteration: parity subset + short bench (tag = $1). Logs in gpurun_out/.
+TAG=${1:-q}
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_frames.py -m gpu -x -q -k "not c2_warm and not 384-12-15-5-7" > gpurun_out/${TAG}_pytest.log 2>&1; echo "pytest_rc=$?" >> gpurun_out/${TAG}_pytest.log
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_bench.log 2>&1
+tail -3 gpurun_out/${TAG}_pytest.log
+tail -1 gpurun_out/${TAG}_bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('fps',d['value'],'e2e',d['e2e']['value'],d['latency_ms'],{k:(v['ms'],v['launches']) for k,v in d['roofline']['kernels'].items()})"
