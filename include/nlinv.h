@@ -61,7 +61,9 @@ typedef struct {
   int fov_full;         /* must be 0: Omega = centred n x n (the whole-grid variant exists only in the
                            oracle's closed-form pins; ERR_ARG here) */
   int rank, world;      /* coil shard of this process; default 0, 1 */
-  const unsigned char* nccl_id;  /* 128-byte ncclUniqueId from nlinv_get_unique_id (rank 0), when world > 1 */
+  const unsigned char* nccl_id;  /* world > 1: 128-byte ncclUniqueId from nlinv_get_unique_id (rank 0) for
+                                    the NCCL transport, or NULL for the peer-memory exchange
+                                    (nlinv_plan_connect*, the default of bench.py) */
 } nlinv_params;
 
 typedef struct {
@@ -98,13 +100,16 @@ nlinv_status nlinv_radial_mask(int nx, int ny, int spokes, int turns, int frame,
 /* Create a plan on the CURRENT CUDA device.
  * nx, ny: grid (must be equal, see conventions). ncoils: total coils J over all ranks (1..256).
  * mask: host uint8 [ny][nx] sampling pattern P_k (nonzero = sampled); copied.
- * p: NULL = defaults. With world > 1 the plan creates its own NCCL communicator from p->nccl_id
- *    (collective: every rank must call). Allocates the whole workspace (no allocation later).
+ * p: NULL = defaults. With world > 1 and p->nccl_id the plan creates its own NCCL communicator
+ *    (collective: every rank must call) and runs the unfused CG passes with NCCL all-reduces; with
+ *    world > 1 and no nccl_id it runs the fused passes with the peer-memory exchange (connect the
+ *    ranks with nlinv_plan_connect* before use). Allocates the whole workspace (no allocation later).
  * out: receives the plan. */
 nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint8_t* mask, const nlinv_params* p,
                                nlinv_plan* out);
 
-/* Replace the plan's P_k. mask_host: host uint8 [ng][ng] (synchronous copy).
+/* Replace the plan's P_k. mask_host: host uint8 [ng][ng] (synchronous copy, after the plan's last
+ * enqueued frame has finished reading the previous P_k).
  * nlinv_plan_set_mask_device: device uint8 [ng][ng], copied on `stream` (per-frame spoke rotation). */
 nlinv_status nlinv_plan_set_mask(nlinv_plan plan, const uint8_t* mask_host);
 nlinv_status nlinv_plan_set_mask_device(nlinv_plan plan, const uint8_t* mask_dev, void* stream);
@@ -215,6 +220,28 @@ nlinv_status nlinv_plan_stats(nlinv_plan plan, nlinv_stats* out);
  * in, out: device [batch][ng][ng]; in == out allowed. */
 nlinv_status nlinv_debug_fft2d(nlinv_plan plan, const nlinv_c32* in, nlinv_c32* out, int batch, int inverse,
                                void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Peer-memory exchange of the coil-sharded multi-GPU path (PAPER P:246
+ * "rho = sum^G rho_g", P:280-289 the peer-to-peer all-reduce kernel, P:339 the exchange inside
+ * DF^H, P:370 other decompositions). A plan created with world > 1 and nccl_id == NULL owns an
+ * exchange window in device memory; every rank's K4 pass writes its coil-sum plane there and the
+ * consumers (the fused K5 + CG pass, the Newton right-hand side) read all ranks' planes over
+ * NVLink in ascending rank order, with the CG dot products exchanged the same way inside the fused
+ * pass (no NCCL call inside a frame; rho replicas stay bit-identical: the replicated rho parts of
+ * the dots are taken from rank 0). Before the first operator call every rank connects to all
+ * ranks' windows (ERR_STATE otherwise):
+ *   nlinv_plan_exchange_handle: the 64-byte cudaIpcMemHandle_t of this plan's window (to be
+ *     exchanged by the caller, e.g. torch.distributed all_gather_object);
+ *   nlinv_plan_connect: handles = world * 64 bytes in rank order (own entry ignored); opens them;
+ *   nlinv_plan_connect_local: plans = the world plans of this job in rank order, all in this
+ *     process (same or peer-accessible devices; tests and single-process drivers).
+ * Requires the rank's coils to fit one fused K5 wave and one K4 chunk (ERR_SIZE at plan creation)
+ * and world <= 8. All ranks must run the same sequence of calls (the exchanges are matched by
+ * per-kind epoch counters). ERR_STATE if the plan is not a peer-memory plan or already connected. */
+nlinv_status nlinv_plan_exchange_handle(nlinv_plan plan, unsigned char handle[64]);
+nlinv_status nlinv_plan_connect(nlinv_plan plan, const unsigned char* handles);
+nlinv_status nlinv_plan_connect_local(nlinv_plan plan, const nlinv_plan* plans);
 
 /* Debug: how many thread-block clusters of the cluster-fused K2 -> K3 -> K4 pass (one cluster per
  * coil, DSMEM transposes) can be co-resident on the current device at grid size ng

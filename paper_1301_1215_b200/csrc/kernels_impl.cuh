@@ -181,6 +181,68 @@ __device__ __forceinline__ void grid_sync_flip(unsigned* bar, unsigned nb, bool 
   __syncthreads();
 }
 
+// ------------------------------------------------------------------ peer-memory exchange primitives (f1)
+__device__ __forceinline__ unsigned long long* xw_flag(char* w, int k) { return reinterpret_cast<unsigned long long*>(w + 128 * k); }
+__device__ __forceinline__ unsigned* xw_counter(char* w, int k) { return reinterpret_cast<unsigned*>(w + 1024 + 128 * k); }
+__device__ __forceinline__ double* xw_dots(char* w, int par) { return reinterpret_cast<double*>(w + 2048) + 8 * par; }
+__device__ __forceinline__ double* xw_xs(char* w) { return reinterpret_cast<double*>(w + 2304); }
+__device__ __forceinline__ float2* xw_S(char* w, int par, size_t Q) { return reinterpret_cast<float2*>(w + kXWinHdr) + (size_t)par * Q; }
+__device__ __forceinline__ float* xw_rss(char* w, size_t Q) { return reinterpret_cast<float*>(w + kXWinHdr + 2 * Q * 8); }
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+// this rank's current epoch of kind k (only this rank writes its own flags)
+__device__ __forceinline__ unsigned long long x_epoch(const XPeers& xp, int k) {
+  return ld_acquire_sys64(xw_flag(xp.win[xp.rank], k));
+}
+// one thread: publish epoch e of kind k (the data of e are written and fenced by the caller)
+__device__ __forceinline__ void x_publish(const XPeers& xp, int k, unsigned long long e) {
+  __threadfence_system();
+  st_release_sys64(xw_flag(xp.win[xp.rank], k), e);
+}
+// one thread: wait until every rank published epoch >= e of kind k
+__device__ __forceinline__ void x_wait_all(const XPeers& xp, int k, unsigned long long e) {
+  for (int h = 0; h < xp.G; ++h) {
+    const unsigned long long* f = xw_flag(xp.win[h], k);
+    unsigned spins = 0;
+    while (ld_acquire_sys64(f) < e) {
+      __nanosleep(64);
+      if (++spins > (1u << 27)) __trap();   // a peer never arrived: abort the context, never hang
+    }
+  }
+}
+// every thread of every CTA: the last CTA of the grid to arrive publishes the next epoch of kind k
+// (all CTAs' writes of that epoch's data precede it)
+__device__ __forceinline__ void x_publish_last_block(const XPeers& xp, int k) {
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned nblk = gridDim.x * gridDim.y * gridDim.z;
+    const unsigned t = atomicAdd(xw_counter(xp.win[xp.rank], k), 1u);
+    s_last = (t == nblk - 1);
+    if (s_last) {
+      *xw_counter(xp.win[xp.rank], k) = 0u;
+      __threadfence();
+      x_publish(xp, k, x_epoch(xp, k) + 1);
+    }
+  }
+  __syncthreads();
+}
+// sum_g S_g[o] over the ranks' published coil-sum planes of epoch e, ascending rank order
+__device__ __forceinline__ float2 x_sum_S(const XPeers& xp, unsigned long long e, size_t Q, size_t o) {
+  float2 sv = make_float2(0.f, 0.f);
+  const int par = (int)(e & 1ull);
+  for (int h = 0; h < xp.G; ++h) sv = cadd(sv, xw_S(xp.win[h], par, Q)[o]);
+  return sv;
+}
+
 // Textbook CG scalars (R9): gamma_i = rr_i / <p_i, A p_i>, beta_i = rr_{i+1} / rr_i.
 // rr_i and <p_i, A p_i> are published as (rho, chat) parts; rho is replicated and counted once.
 __device__ __forceinline__ double cg_rr(const double* scal, int i) { return scal[SC_RR_RHO + i] + scal[SC_RR_CHAT + i]; }
@@ -309,7 +371,8 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
           float2 sv = make_float2(0.f, 0.f);
           if (xx >= q && xx < q + n && y >= q && y < q + n) {
             const size_t o = (size_t)(y - q) * n + (xx - q);
-            for (int sp = 0; sp < a.nS; ++sp) sv = cadd(sv, a.S[sp * Qs + o]);
+            if (a.xp.G > 0) sv = x_sum_S(a.xp, x_epoch(a.xp, XK_S), Qs, o);   // ranks' planes, rank order
+            else for (int sp = 0; sp < a.nS; ++sp) sv = cadd(sv, a.S[sp * Qs + o]);
           }
           if constexpr (MODE == CK_FFT_W_NORMAL) {
             const float2 pv = a.rho_a[i];
@@ -582,6 +645,12 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColAr
   }
   pdl_wait();
   pdl_trigger();
+  if constexpr (MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ) {
+    if (a.xp.G > 0) {   // peer exchange: every rank's K4 has published its coil-sum plane
+      if (threadIdx.x == 0) x_wait_all(a.xp, XK_S, x_epoch(a.xp, XK_S));
+      __syncthreads();
+    }
+  }
   if constexpr (MODE == CK_IFFT_W_CG) {
     if (a.cg1) {
       if (a.iter > 0) cg1_gamma_beta(a.scal, a.iter - 1, &a.gamma, &a.beta);
@@ -656,6 +725,14 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   }
   pdl_wait();
   pdl_trigger();
+  // peer exchange: wait for every rank's coil-sum plane of this iteration (published by its K4)
+  unsigned long long eS = 0, eD = 0;
+  if (a.xp.G > 0) {
+    eS = x_epoch(a.xp, XK_S);
+    eD = x_epoch(a.xp, XK_DOTS) + 1;   // read before CTA 0 publishes it (after the grid barrier)
+    if (tid == 0) x_wait_all(a.xp, XK_S, eS);
+    __syncthreads();
+  }
 
   // prologue: T4 (Omega rows only; the others are zero)
   float2 v[E];
@@ -687,7 +764,8 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
     float2 sv = make_float2(0.f, 0.f);
     if (xx >= q && xx < q + n && y >= q && y < q + n) {
       const size_t o = (size_t)(y - q) * n + (xx - q);
-      for (int s2 = 0; s2 < a.nS; ++s2) sv = cadd(sv, a.S[s2 * Qs + o]);
+      if (a.xp.G > 0) sv = x_sum_S(a.xp, eS, Qs, o);   // the ranks' coil-sum planes, rank order
+      else for (int s2 = 0; s2 < a.nS; ++s2) sv = cadd(sv, a.S[s2 * Qs + o]);
     }
     return sv;
   };
@@ -698,7 +776,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
       const size_t i = lo + tid + (size_t)u * blockDim.x;
       const bool ok = i < hi;
       sp[u] = ok ? a.rho_a[i] : make_float2(0.f, 0.f);
-      sr[u] = (ok && !last) ? a.rho_r[i] : make_float2(0.f, 0.f);
+      sr[u] = ok ? a.rho_r[i] : make_float2(0.f, 0.f);
       sv[u] = ok ? stripe_sum(i) : make_float2(0.f, 0.f);
     }
 #pragma unroll
@@ -718,11 +796,11 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
       const float2 o = make_float2(fmaf(a.alpha, pv.x, sv.x), fmaf(a.alpha, pv.y, sv.y));
       a.rho_out[i] = o;
       d[0] += (double)pv.x * o.x + (double)pv.y * o.y;
+      const float2 rv = a.rho_r[i];
+      d[6] += (double)rv.x * rv.x + (double)rv.y * rv.y;
       if (!last) {
-        const float2 rv = a.rho_r[i];
         d[2] += (double)rv.x * o.x + (double)rv.y * o.y;
         d[4] += (double)o.x * o.x + (double)o.y * o.y;
-        d[6] += (double)rv.x * rv.x + (double)rv.y * rv.y;
       }
     }
   }
@@ -755,11 +833,12 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
         v[e0 + u] = o;
         buf(k) = pv[u];
         d[1] += (double)pv[u].x * o.x + (double)pv[u].y * o.y;
+        // <r_i, r_i> directly from the stored r_i in every iteration (R19); the last one reads r here
+        const float2 rv = last ? a.r[j * N + (size_t)k * L + x] : pf[k * CW + c];
+        d[7] += (double)rv.x * rv.x + (double)rv.y * rv.y;
         if (!last) {
-          const float2 rv = pf[k * CW + c];
           d[3] += (double)rv.x * o.x + (double)rv.y * o.y;
           d[5] += (double)o.x * o.x + (double)o.y * o.y;
-          d[7] += (double)rv.x * rv.x + (double)rv.y * rv.y;
         }
       }
     }
@@ -794,10 +873,35 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
     }
     __syncthreads();
   }
-  // <r_i, r_i>: computed in this pass; the last iteration (no r read) takes the previous pass's value
+  if (a.xp.G > 0) {
+    // peer exchange of the dots (one epoch of kind XK_DOTS): CTA 0 publishes this rank's totals; every
+    // CTA waits for all ranks and forms the global totals in the same order on every rank: the chat
+    // parts summed over ranks (ascending), the replicated rho parts taken from rank 0, so gamma and
+    // beta -- and with them the rho replicas -- are bit-identical on all ranks
+    if (bid == 0 && tid == 0) {
+      double* dd = xw_dots(a.xp.win[a.xp.rank], (int)(eD & 1ull));
+      for (int k = 0; k < NV; ++k) dd[k] = red[k];
+      x_publish(a.xp, XK_DOTS, eD);
+    }
+    if (tid == 0) x_wait_all(a.xp, XK_DOTS, eD);
+    __syncthreads();
+    double gk = 0.0;
+    if (tid < NV) {
+      const int par = (int)(eD & 1ull);
+      if ((tid & 1) == 0) {
+        gk = __ldcv(xw_dots(a.xp.win[0], par) + tid);
+      } else {
+        for (int h = 0; h < a.xp.G; ++h) gk += __ldcv(xw_dots(a.xp.win[h], par) + tid);
+      }
+    }
+    __syncthreads();
+    if (tid < NV) red[tid] = gk;
+    __syncthreads();
+  }
+  // <r_i, r_i>: computed in this pass from the stored r_i (R19)
   trace_stamp(a.trace, 5);   // post-barrier totals done
-  const double rr_r = last ? a.scal[SC_RR_RHO + a.iter] : red[6];
-  const double rr_c = last ? a.scal[SC_RR_CHAT + a.iter] : red[7];
+  const double rr_r = red[6];
+  const double rr_c = red[7];
   const double rr = rr_r + rr_c;
   const double pap = red[0] + red[1];
   const float gamma = (rr != 0.0) ? (float)(rr / pap) : 0.0f;
@@ -807,12 +911,10 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
     const double nr = fmax(rr_r - 2.0 * g * red[2] + g * g * red[4], 0.0);
     const double nc = fmax(rr_c - 2.0 * g * red[3] + g * g * red[5], 0.0);
     beta = (rr != 0.0) ? (float)((nr + nc) / rr) : 0.0f;
-    if (bid == 0 && tid == 0) {
-      a.scal_w[SC_RR_RHO + a.iter] = rr_r;
-      a.scal_w[SC_RR_CHAT + a.iter] = rr_c;
-      a.scal_w[SC_RR_RHO + a.iter + 1] = nr;
-      a.scal_w[SC_RR_CHAT + a.iter + 1] = nc;
-    }
+  }
+  if (bid == 0 && tid == 0) {   // the direct <r_i, r_i> (the next pass overwrites slot i + 1 with its own)
+    a.scal_w[SC_RR_RHO + a.iter] = rr_r;
+    a.scal_w[SC_RR_CHAT + a.iter] = rr_c;
   }
   if (bid == 0 && tid == 0) {
     a.scal_w[SC_PAP_RHO + a.iter] = red[0];
@@ -1216,7 +1318,16 @@ __global__ void __launch_bounds__(256, NLV_MINB) row_kernel(RowArgs a, const flo
     // CTA = (Omega row, chunk of a.kchunk coils); chunk c writes coil-sum plane c. rho|Omega and
     // c_j|Omega (fixed for the Newton step) are read before griddepcontrol.wait
     const int jlo = blockIdx.y * a.kchunk, jhi = min(a.J, jlo + a.kchunk);
-    row_task_k4<L>(a, blockIdx.x, jlo, jhi, blockIdx.y, tw, xb, xb + (size_t)L * (blockDim.x / Cfg<L>::T), true, true);
+    if (a.xp.G > 0) {
+      // peer exchange: the rank's coil-sum plane (one chunk = all local coils) goes straight into
+      // the exchange window's buffer of the next epoch; the last CTA publishes it
+      RowArgs b = a;
+      b.S = xw_S(a.xp.win[a.xp.rank], (int)((x_epoch(a.xp, XK_S) + 1) & 1ull), (size_t)(L / 2) * (L / 2));
+      row_task_k4<L>(b, blockIdx.x, jlo, jhi, 0, tw, xb, xb + (size_t)L * (blockDim.x / Cfg<L>::T), true, true);
+      x_publish_last_block(a.xp, XK_S);
+    } else {
+      row_task_k4<L>(a, blockIdx.x, jlo, jhi, blockIdx.y, tw, xb, xb + (size_t)L * (blockDim.x / Cfg<L>::T), true, true);
+    }
   } else if constexpr (MODE == RK_K2) {
     // per-group staging of c_j|Omega, rho|Omega, p_rho|Omega after the exchange buffers (RowGeo::SMEM_K2)
     const int gpc = blockDim.x / Cfg<L>::T;

@@ -61,7 +61,11 @@ struct nlinv_plan_s {
   float2 *S_all = nullptr, *S = nullptr, *S_sum = nullptr;   // per-coil terms; local sum; rank sum
   float *rss_all = nullptr, *rss = nullptr, *rss_sum = nullptr;
   int trace_mode = -1;                    // debug: column mode whose CTA timelines are recorded
-  bool multi = false;                     // collective code path (world > 1 or NLINV_FORCE_NCCL=1)
+  bool multi = false;                     // NCCL collective code path (world > 1 with an NCCL id, or NLINV_FORCE_NCCL=1)
+  bool p2p = false;                       // peer-memory exchange (world > 1 without an NCCL id)
+  XPeers xp{};                            // connected peers (xp.G == 0 until nlinv_plan_connect*)
+  char* xwin = nullptr;                   // this rank's exchange window (IPC-exportable)
+  std::vector<void*> ipc_open;            // peer windows opened through CUDA IPC
   bool fused = false;                     // fused K5 + CG + K1 pass, one grid barrier (k5cg_kernel, R19)
   bool k234 = false;                      // cluster-fused K2 -> K3 -> K4 in the fused CG loop (k234_kernel)
   bool cg1 = false;                       // unfused CG: one (grouped) scalar all-reduce per iteration (R19)
@@ -455,6 +459,8 @@ static void plan_free(nlinv_plan pl) {
   for (float* p : pl->tr_pw) cudaFree(p);
   cudaFree(pl->h_raw);
   cudaFree(pl->pw_buf);
+  for (void* w : pl->ipc_open) cudaIpcCloseMemHandle(w);
+  cudaFree(pl->xwin);
   if (pl->slab) {   // tA, tB, dx, r, p, c_omega live in one slab
     cudaFree(pl->slab);
     pl->tA = pl->tB = pl->dx = pl->r = pl->p = pl->c_omega = nullptr;
@@ -491,9 +497,10 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
   if (prm.world > ncoils) return fail(pl, NLINV_ERR_SIZE, "more ranks than coils");
   if (!(prm.q > 0.0f) || !(prm.alpha0 > 0.0f)) return fail(pl, NLINV_ERR_ARG, "alpha0 and q must be > 0");
 #ifndef NLINV_WITH_NCCL
-  if (prm.world > 1) return fail(pl, NLINV_ERR_NOT_BUILT, "built without NCCL");
+  if (prm.world > 1 && prm.nccl_id) return fail(pl, NLINV_ERR_NOT_BUILT, "built without NCCL");
 #endif
-  if (prm.world > 1 && !prm.nccl_id) return fail(pl, NLINV_ERR_ARG, "world > 1 needs nccl_id");
+  if (prm.world > kMaxRanks && !prm.nccl_id)
+    return fail(pl, NLINV_ERR_SIZE, "the peer-memory exchange supports at most 8 ranks (one node)");
   if (prm.fov_full) return fail(pl, NLINV_ERR_ARG, "fov_full is an oracle-only test mode (Omega pruning is structural)");
   {
     int dev = -1;
@@ -517,11 +524,12 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
     // exercised and parity-tested on a single device)
     const char* fn = std::getenv("NLINV_FORCE_NCCL");
 #ifdef NLINV_WITH_NCCL
-    pl->multi = prm.world > 1 || (fn && fn[0] == '1');
+    pl->multi = (prm.world > 1 && p->nccl_id != nullptr) || (prm.world == 1 && fn && fn[0] == '1');
 #else
     pl->multi = false;
     (void)fn;
 #endif
+    pl->p2p = prm.world > 1 && !pl->multi;
   }
   nlinv_coil_partition(ncoils, prm.world, prm.rank, &pl->first, &pl->count);
   pl->J = pl->count;
@@ -591,6 +599,15 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
       ok &= alloc((void**)&pl->kpart, sizeof(double) * 8 * kMaxRedBlocks);
     }
   }
+  if (pl->p2p) {
+    // the peer-memory path runs the fused CG pass on every rank with one coil-sum plane per rank
+    if (!pl->fused || k4_planes(nx, pl->J) != 1) {
+      plan_free(pl);
+      return fail(nullptr, NLINV_ERR_SIZE, "peer-memory exchange: the rank's coils do not fit one fused wave / one K4 chunk");
+    }
+    ok &= alloc((void**)&pl->xwin, xwin_bytes(pl->Q));
+    ok &= alloc((void**)&pl->rss_sum, sizeof(float) * pl->Q);
+  }
   ok &= alloc((void**)&pl->scal, sizeof(double) * SC_TOTAL);
   ok &= alloc((void**)&pl->partials, sizeof(double) * 8 * kMaxRedBlocks);
   ok &= alloc((void**)&pl->counter, sizeof(unsigned) * 4);
@@ -621,6 +638,7 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
   if (e == cudaSuccess) e = cudaMemset(pl->scal, 0, sizeof(double) * SC_TOTAL);
   if (e == cudaSuccess) e = cudaMemset(pl->counter, 0, sizeof(unsigned) * 4);
   if (e == cudaSuccess && pl->kbar) e = cudaMemset(pl->kbar, 0, sizeof(unsigned) * 4);
+  if (e == cudaSuccess && pl->xwin) e = cudaMemset(pl->xwin, 0, xwin_bytes(pl->Q));
   if (e != cudaSuccess) {
     std::string msg = std::string("plan upload: ") + cudaGetErrorString(e);
     plan_free(pl);
@@ -649,6 +667,9 @@ extern "C" nlinv_status nlinv_plan_set_mask(nlinv_plan pl, const uint8_t* mask_h
   if (!pl || !mask_host) return fail(pl, NLINV_ERR_ARG, "NULL argument");
   std::vector<uint8_t> m8(pl->N);
   for (size_t i = 0; i < pl->N; ++i) m8[i] = mask_host[i] ? 1 : 0;
+  // the previous frame's work (possibly on a non-blocking stream) may still read P_k
+  if (pl->last_stream) CU(cudaStreamSynchronize(pl->last_stream));
+  if (pl->gstream) CU(cudaStreamSynchronize(pl->gstream));
   CU(cudaMemcpy(pl->mask, m8.data(), pl->N, cudaMemcpyHostToDevice));
   pl->mnnz_host = -1;
   pl->pw_active = nullptr;   // a binary P_k replaces any KB weights
@@ -720,6 +741,7 @@ struct Enq {
     a.scal_w = pl->scal;
     a.counter = pl->counter;
     a.J = pl->J;
+    a.xp = pl->xp;
     const char* name = kColNames[mode];
     if (mode == CK_FFT_W_RHS && a.fuse_k1) name = "col_rhs_k1";
     if (mode == CK_K5CG) name = a.fuse_k1 ? "col_k5_cg_k1" : "col_k5_newton";
@@ -727,6 +749,7 @@ struct Enq {
   }
   nlinv_status row(int mode, RowArgs a) {
     a.J = pl->J;
+    if (mode == RK_K4) a.xp = pl->xp;
     a.c_omega = pl->c_omega;
     a.rho_omega = pl->rho_omega;
     return kern(kRowNames[mode], [&] { return launch_row(pl->ng, mode, a, pl->tw, s); });
@@ -836,7 +859,7 @@ nlinv_status enq_k4_allreduce(Enq& q) {
   ra.in = pl->tA;
   ra.out = pl->tB;
   ra.S = pl->S_all;   // one plane per K4 coil chunk
-  TRY(q.row(RK_K4, ra));
+  TRY(q.row(RK_K4, ra));   // peer exchange: K4 writes its plane into the window and publishes it
   if (pl->multi) {
     const int np = k4_planes(pl->ng, pl->J);
     TRY(q.kern("coil_sum", [&] { return launch_coil_sum(pl->ng, pl->S_all, np, pl->S, q.s); }));
@@ -891,6 +914,21 @@ nlinv_status enq_normal(Enq& q, float alpha, const float2* dx, float2* out, bool
     TRY(q.allreduce_scalar(SC_PAP_CHAT + iter));   // chat part; the rho part is replicated
   }
   return NLINV_OK;
+}
+
+// peer exchange at the end of a frame: ||P y - F(x_n)||^2 of every Newton step summed over the
+// ranks (SC_RES slots, in place) and, with rss_out, the RSS plane summed over the ranks
+nlinv_status enq_xchg_frame(Enq& q, int K, float* rss_out) {
+  nlinv_plan pl = q.pl;
+  XchgArgs xa{};
+  xa.xp = pl->xp;
+  xa.scal = pl->scal;
+  xa.nsum = K < 64 ? K : 64;
+  xa.nr0 = 0;
+  for (int n = 0; n < xa.nsum; ++n) xa.src[n] = xa.dst[n] = SC_RES + n;
+  xa.rss_out = rss_out;
+  xa.Q = (int)pl->Q;
+  return q.kern("xchg", [&] { return launch_xchg(xa, q.s); });
 }
 
 // the whole frame: K Newton steps of L CG iterations on x (in place)
@@ -1033,13 +1071,20 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
     ra.xrho = x;
     ra.rss = pl->rss_all;
     TRY(q.row(RK_RSS, ra));
-    if (pl->multi) {
+    if (pl->p2p) {   // local RSS into the window, then one two-phase exchange (+ the residual history)
+      float* wrss = reinterpret_cast<float*>(pl->xwin + kXWinHdr + 2 * pl->Q * sizeof(float2));
+      TRY(q.kern("rss_sum", [&] { return launch_rss_sum(pl->ng, pl->rss_all, pl->J, wrss, q.s); }));
+      TRY(enq_xchg_frame(q, K, pl->rss_sum));
+      TRY(q.kern("image", [&] { return launch_image(pl->ng, pl->rho_omega, pl->rss_sum, 1, img, q.s); }));
+    } else if (pl->multi) {
       TRY(q.kern("rss_sum", [&] { return launch_rss_sum(pl->ng, pl->rss_all, pl->J, pl->rss, q.s); }));
       TRY(q.allreduce_f(pl->rss, pl->rss_sum, pl->Q));
       TRY(q.kern("image", [&] { return launch_image(pl->ng, pl->rho_omega, pl->rss_sum, 1, img, q.s); }));
     } else {
       TRY(q.kern("image", [&] { return launch_image(pl->ng, pl->rho_omega, pl->rss_all, pl->J, img, q.s); }));
     }
+  } else if (pl->p2p) {
+    TRY(enq_xchg_frame(q, K, nullptr));   // the residual history is a sum over all ranks' coils
   }
   return NLINV_OK;
 }
@@ -1089,6 +1134,7 @@ extern "C" nlinv_status nlinv_apply_derivative(nlinv_plan pl, const nlinv_c32* d
 extern "C" nlinv_status nlinv_apply_adjoint(nlinv_plan pl, const nlinv_c32* dy, nlinv_c32* dx, void* stream) {
   if (!pl || !dy || !dx) return fail(pl, NLINV_ERR_ARG, "NULL argument");
   if (!pl->point_set) return fail(pl, NLINV_ERR_STATE, "adjoint before set_point");
+  if (pl->p2p && pl->xp.G == 0) return fail(pl, NLINV_ERR_STATE, "peer-memory plan used before nlinv_plan_connect");
   Enq q{pl, (cudaStream_t)stream};
   auto body = [&]() -> nlinv_status {
     ColArgs ca{};
@@ -1114,6 +1160,7 @@ extern "C" nlinv_status nlinv_apply_normal(nlinv_plan pl, float alpha, const nli
   if (!pl || !dx || !out) return fail(pl, NLINV_ERR_ARG, "NULL argument");
   if (dx == out) return fail(pl, NLINV_ERR_ARG, "dx and out must not overlap");
   if (!pl->point_set) return fail(pl, NLINV_ERR_STATE, "normal before set_point");
+  if (pl->p2p && pl->xp.G == 0) return fail(pl, NLINV_ERR_STATE, "peer-memory plan used before nlinv_plan_connect");
   Enq q{pl, (cudaStream_t)stream};
   nlinv_status st = enq_normal(q, alpha, (const float2*)dx, (float2*)out, false, 0);
   pl->launches += q.kernels;
@@ -1141,6 +1188,7 @@ extern "C" nlinv_status nlinv_reconstruct(nlinv_plan pl, const nlinv_c32* frame,
   if (!pl || !frame || !x_out) return fail(pl, NLINV_ERR_ARG, "NULL argument");
   if (newton_steps < 0 || newton_steps > kMaxNewton) return fail(pl, NLINV_ERR_SIZE, "newton_steps out of range");
   if (cg_iters < 1 || cg_iters > kMaxCG) return fail(pl, NLINV_ERR_SIZE, "cg_iters out of range");
+  if (pl->p2p && pl->xp.G == 0) return fail(pl, NLINV_ERR_STATE, "peer-memory plan used before nlinv_plan_connect");
   cudaStream_t us = (cudaStream_t)stream;
   // A CUDA graph cannot be captured on the legacy default stream: callers on it (e.g. torch's
   // default stream) get the frame's graph on a plan-owned stream fenced by events on both sides,
@@ -1451,3 +1499,64 @@ extern "C" nlinv_status nlinv_stream_frame_radial(nlinv_plan pl, const nlinv_c32
 
 // debug: co-resident clusters of the cluster-fused K2-K3-K4 kernel at grid size ng (< 0: not built)
 extern "C" int nlinv_debug_k234_clusters(int ng) { return k234_max_clusters(ng); }
+
+// ------------------------------------------------------------------ peer-memory exchange
+extern "C" nlinv_status nlinv_plan_exchange_handle(nlinv_plan pl, unsigned char handle[64]) {
+  if (!pl || !handle) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  if (!pl->p2p) return fail(pl, NLINV_ERR_STATE, "not a peer-memory plan (world == 1 or NCCL transport)");
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t size");
+  CU(cudaIpcGetMemHandle(&h, pl->xwin));
+  std::memcpy(handle, &h, 64);
+  return NLINV_OK;
+}
+
+static nlinv_status connect_done(nlinv_plan pl) {
+  pl->xp.G = pl->world;
+  pl->xp.rank = pl->rank;
+  if (pl->gexec) {   // a graph captured before the peers were known is stale
+    cudaGraphExecDestroy(pl->gexec);
+    pl->gexec = nullptr;
+  }
+  return NLINV_OK;
+}
+
+extern "C" nlinv_status nlinv_plan_connect(nlinv_plan pl, const unsigned char* handles) {
+  if (!pl || !handles) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  if (!pl->p2p) return fail(pl, NLINV_ERR_STATE, "not a peer-memory plan (world == 1 or NCCL transport)");
+  if (pl->xp.G) return fail(pl, NLINV_ERR_STATE, "already connected");
+  for (int r = 0; r < pl->world; ++r) {
+    if (r == pl->rank) {
+      pl->xp.win[r] = pl->xwin;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles + 64 * r, 64);
+    void* ptr = nullptr;
+    CU(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    pl->ipc_open.push_back(ptr);
+    pl->xp.win[r] = static_cast<char*>(ptr);
+  }
+  return connect_done(pl);
+}
+
+extern "C" nlinv_status nlinv_plan_connect_local(nlinv_plan pl, const nlinv_plan* plans) {
+  if (!pl || !plans) return fail(pl, NLINV_ERR_ARG, "NULL argument");
+  if (!pl->p2p) return fail(pl, NLINV_ERR_STATE, "not a peer-memory plan (world == 1 or NCCL transport)");
+  if (pl->xp.G) return fail(pl, NLINV_ERR_STATE, "already connected");
+  for (int r = 0; r < pl->world; ++r) {
+    const nlinv_plan o = plans[r];
+    if (!o || !o->p2p || o->rank != r || o->world != pl->world || o->ng != pl->ng)
+      return fail(pl, NLINV_ERR_ARG, "plans[] must be this job's peer-memory plans in rank order");
+    if (o->device != pl->device) {   // another GPU of this process: direct peer access over NVLink
+      int can = 0;
+      CU(cudaDeviceCanAccessPeer(&can, pl->device, o->device));
+      if (!can) return fail(pl, NLINV_ERR_CUDA, "no peer access between the plans' devices");
+      cudaError_t e = cudaDeviceEnablePeerAccess(o->device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CU(e);
+      cudaGetLastError();
+    }
+    pl->xp.win[r] = o->xwin;
+  }
+  return connect_done(pl);
+}

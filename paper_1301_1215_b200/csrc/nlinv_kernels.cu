@@ -96,6 +96,48 @@ __global__ void image_kernel(const float2* __restrict__ rho_omega, const float* 
   }
 }
 
+// generic two-phase peer exchange (see XPeers): arrive with this rank's scalars in its
+// window, wait for every rank, reduce (sums in ascending rank order, or rank 0's value for the
+// replicated rho parts), ack, wait for every rank's ack (every window buffer is reusable after it)
+__global__ void __launch_bounds__(1024) xchg_kernel(XchgArgs a) {
+  __shared__ unsigned long long s_e;
+  pdl_wait();
+  char* own = a.xp.win[a.xp.rank];
+  const int nv = a.nsum + a.nr0;
+  double* xs = xw_xs(own);
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) xs[i] = a.scal[a.src[i]];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long e = x_epoch(a.xp, XK_A) + 1;
+    x_publish(a.xp, XK_A, e);
+    x_wait_all(a.xp, XK_A, e);
+    s_e = e;
+  }
+  __syncthreads();
+  double val = 0.0;
+  if ((int)threadIdx.x < a.nsum) {
+    for (int h = 0; h < a.xp.G; ++h) val += __ldcv(xw_xs(a.xp.win[h]) + threadIdx.x);
+  } else if ((int)threadIdx.x < nv) {
+    val = __ldcv(xw_xs(a.xp.win[0]) + threadIdx.x);
+  }
+  if (a.rss_out != nullptr) {
+    for (int i = threadIdx.x; i < a.Q; i += blockDim.x) {
+      float sacc = 0.f;
+      for (int h = 0; h < a.xp.G; ++h) sacc += __ldcv(xw_rss(a.xp.win[h], (size_t)a.Q) + i);
+      a.rss_out[i] = sacc;
+    }
+  }
+  if ((int)threadIdx.x < nv) a.scal[a.dst[threadIdx.x]] = val;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    x_publish(a.xp, XK_B, s_e);
+    x_wait_all(a.xp, XK_B, s_e);
+  }
+}
+cudaError_t launch_xchg(const XchgArgs& a, cudaStream_t s) {
+  return launch_k(xchg_kernel, dim3(1), dim3(1024), 0, s, a);
+}
+
 // local coil sums before the cross-rank all-reduce (world > 1)
 __global__ void coil_sum_kernel(const float2* __restrict__ S_all, int J, float2* S, int Q) {
   pdl_wait();

@@ -47,6 +47,31 @@ enum RowMode {
   RK_K4,            // row IFFT -> u; S += conj(c) u; v = conj(rho) u -> row FFT
 };
 
+// ------------------------------------------------------------------ peer-memory exchange
+// The coil-sharded multi-GPU path's exchanges go through every rank's exchange window, a device
+// allocation the other ranks map (CUDA IPC between processes, plain pointers inside one process):
+// the modern analogue of the paper's peer-to-peer all-reduce kernel kern_all_red_p2p_2d
+// (P:280-289), with loads over NVLink instead of PCIe copies, fused into the kernels that produce
+// and consume the data.
+//   kind XK_S:    the local coil-sum plane of the Omega window (K4 output), double-buffered by epoch
+//   kind XK_DOTS: the fused K5 pass's 8 dot partials (rho, chat parts), double-buffered by epoch
+//   kinds XK_A/B: arrive / ack flags of the generic two-phase exchange (xchg_kernel)
+// A rank publishes epoch e of kind k by a release store of e into its own flag k after the data of
+// e are written; a consumer waits (acquire loads) until every rank's flag k >= e and then reads every
+// rank's buffer [e % 2] in ascending rank order. Double buffering is safe because a rank produces
+// epoch e only after it consumed e - 1, i.e. after every peer published e - 1, which every peer does
+// only after it finished reading e - 2 (stream order).
+constexpr int kMaxRanks = 8;
+enum XKind { XK_S = 0, XK_DOTS = 1, XK_A = 2, XK_B = 3, XK_COUNT = 4 };
+struct XPeers {
+  char* win[kMaxRanks];    // every rank's exchange window, [rank] = this rank's own
+  int G;                   // ranks (0: exchange off)
+  int rank;
+};
+constexpr size_t kXWinHdr = 4096;   // flags [kind * 128], counters [1024 + kind * 128], dots [2048], xs [2304]
+constexpr int kXsSlots = 192;       // generic exchange scalars (doubles)
+inline size_t xwin_bytes(size_t Q) { return kXWinHdr + 2 * Q * 8 + Q * 4; }
+
 struct ColArgs {
   const float2* in;        // [J][n][ng] half image (Omega rows) or full k-space input
   float2* out;             // [J][n][ng] half image, or [J][ng][ng] k-space output
@@ -88,6 +113,7 @@ struct ColArgs {
                            // K1 applies r -= gamma Ap (A p from src2 / rho_a) before the p update
   float alpha;
   int J;
+  XPeers xp;               // peer-memory exchange (world > 1 without NCCL); xp.G == 0: off
 };
 
 struct RowArgs {
@@ -101,6 +127,7 @@ struct RowArgs {
   float* rss;              // [J][n][n] per-coil |c_j|^2 (RSS)
   const uint8_t* mask;     // [ng][ng] P_k (cluster-fused K2-K3-K4)
   int J;
+  XPeers xp;               // peer-memory exchange: K4 writes its coil-sum plane into the window and publishes
   int kchunk;              // K4 coils per CTA (set by the launcher)
 };
 int k4_planes(int ng, int J);  // number of K4 coil-sum planes
@@ -149,6 +176,18 @@ bool k234_supported(int ng);
 cudaError_t launch_k234(int ng, const RowArgs& a, const float2* tw, cudaStream_t s);
 int k234_max_clusters(int ng);
 cudaError_t launch_coil_sum(int ng, const float2* S_all, int J, float2* S, cudaStream_t s);
+// generic two-phase peer exchange (one CTA): nsum scalars summed over ranks (slots src[i] -> dst[i] of
+// scal), nr0 scalars taken from rank 0, and optionally the RSS plane (rss_local [Q] of every rank summed
+// into rss_out). Arrive, wait, reduce, ack, wait, then write (so every buffer is reusable afterwards).
+struct XchgArgs {
+  XPeers xp;
+  double* scal;
+  int nsum, nr0;
+  int src[64], dst[64];    // first nsum: summed; next nr0: rank 0's value
+  float* rss_out;          // nullptr: no RSS plane
+  int Q;
+};
+cudaError_t launch_xchg(const XchgArgs& a, cudaStream_t s);
 cudaError_t launch_rss_sum(int ng, const float* rss_all, int J, float* rss, cudaStream_t s);
 
 }  // namespace nlv

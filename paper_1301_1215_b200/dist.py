@@ -1,8 +1,9 @@
 """Host-side plumbing of the coil-sharded multi-GPU path (one process per GPU).
 
-torch.distributed only carries the 128-byte NCCL unique id and host metadata; the data path
-collectives (the Omega-window coil-sum all-reduce of P:246 / P:289 and the CG dot products)
-are issued by libnlinv.so on its own NCCL communicator.
+torch.distributed only carries host metadata: the 64-byte CUDA IPC handles of the ranks' exchange
+windows (peer-memory transport, the default) or the 128-byte NCCL unique id (NCCL transport). The
+data-path exchanges (the Omega-window coil sum of P:246 / P:289 and the CG dot products) are done by
+libnlinv.so's own kernels over peer memory, or on its own NCCL communicator.
 """
 from __future__ import annotations
 
@@ -19,6 +20,15 @@ def exchange_unique_id(rank: int, world: int, group=None) -> bytes | None:
     obj = [get_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0, group=group)
     return obj[0]
+
+
+def connect_peers(plan, group=None) -> None:
+    """Peer-memory exchange (world > 1 without an NCCL id): all-gather every rank's 64-byte
+    exchange-window handle over torch.distributed and open them (nlinv_plan_connect)."""
+    import torch.distributed as dist
+    handles = [None] * dist.get_world_size(group)
+    dist.all_gather_object(handles, plan.exchange_handle(), group=group)
+    plan.connect(handles)
 
 
 def local_frame(y_full: np.ndarray, ncoils: int, rank: int, world: int) -> np.ndarray:

@@ -66,6 +66,9 @@ _SIGS = {
     "nlinv_plan_stats": (c_int, [c_void_p, ctypes.POINTER(Stats)]),
     "nlinv_debug_fft2d": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]),
     "nlinv_debug_k234_clusters": (c_int, [c_int]),
+    "nlinv_plan_exchange_handle": (c_int, [c_void_p, ctypes.c_char_p]),
+    "nlinv_plan_connect": (c_int, [c_void_p, ctypes.c_char_p]),
+    "nlinv_plan_connect_local": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
     "nlinv_plan_launch_count": (c_ll, [c_void_p]),
     "nlinv_stream_frame": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]),
     "nlinv_stream_reset": (c_int, [c_void_p]),
@@ -157,6 +160,23 @@ class Plan:
         self.first, self.count = first.value, count.value
         self.n = ng // 2
 
+    # ---------------------------------------------------------------- peer-memory exchange (world > 1, no NCCL id)
+    def exchange_handle(self) -> bytes:
+        """64-byte CUDA IPC handle of this rank's exchange window (nlinv_plan_exchange_handle)."""
+        buf = ctypes.create_string_buffer(64)
+        _check(_lib.nlinv_plan_exchange_handle(self._h, buf), self._h)
+        return buf.raw
+
+    def connect(self, handles):
+        """Open every rank's exchange window; handles: list of world 64-byte handles, rank order."""
+        blob = b"".join(bytes(h) for h in handles)
+        _check(_lib.nlinv_plan_connect(self._h, blob), self._h)
+
+    def connect_local(self, plans):
+        """Connect to the world plans of this process (rank order, including this one)."""
+        arr = (c_void_p * len(plans))(*[p._h.value for p in plans])
+        _check(_lib.nlinv_plan_connect_local(self._h, arr), self._h)
+
     # ---------------------------------------------------------------- shapes
     @property
     def x_shape(self):
@@ -184,12 +204,12 @@ class Plan:
         return torch.empty(shape, dtype=torch.complex64, device="cuda")
 
     # ---------------------------------------------------------------- calls
-    def set_mask(self, mask):
+    def set_mask(self, mask, stream=None):
         import torch
         if isinstance(mask, torch.Tensor) and mask.is_cuda:
             if mask.dtype != torch.uint8 or tuple(mask.shape) != (self.ng, self.ng) or not mask.is_contiguous():
                 raise ValueError("device mask must be contiguous uint8 [ng, ng]")
-            _check(_lib.nlinv_plan_set_mask_device(self._h, c_void_p(mask.data_ptr()), _stream_ptr(None)), self._h)
+            _check(_lib.nlinv_plan_set_mask_device(self._h, c_void_p(mask.data_ptr()), _stream_ptr(stream)), self._h)
             return
         m = np.ascontiguousarray(np.asarray(mask, dtype=np.uint8))
         _check(_lib.nlinv_plan_set_mask(self._h, m.ctypes.data), self._h)

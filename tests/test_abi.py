@@ -73,14 +73,20 @@ def test_plan_create_validates_before_device():
     assert B._lib.nlinv_plan_create(40, 40, 4, m.ctypes.data, None, ctypes.byref(h)) == 2     # unsupported ng
     assert B._lib.nlinv_plan_create(32, 32, 0, m.ctypes.data, None, ctypes.byref(h)) == 2     # no coils
     assert B._lib.nlinv_plan_create(32, 32, 4, None, None, ctypes.byref(h)) == 1              # NULL mask
-    prm.world, prm.rank = 2, 0
-    assert B._lib.nlinv_plan_create(32, 32, 4, m.ctypes.data, ctypes.byref(prm), ctypes.byref(h)) == 1  # no id
+    prm.world, prm.rank = 9, 0   # peer-memory transport (no NCCL id): at most 8 ranks (one node)
+    assert B._lib.nlinv_plan_create(32, 32, 12, m.ctypes.data, ctypes.byref(prm), ctypes.byref(h)) == 2
+    prm.world, prm.rank = 2, 2   # rank out of range
+    assert B._lib.nlinv_plan_create(32, 32, 4, m.ctypes.data, ctypes.byref(prm), ctypes.byref(h)) == 1
     prm.world, prm.rank, prm.fov_full = 1, 0, 1
     assert B._lib.nlinv_plan_create(32, 32, 4, m.ctypes.data, ctypes.byref(prm), ctypes.byref(h)) == 1
     # NULL plan handles are rejected, never dereferenced
     assert B._lib.nlinv_set_point(None, None, None) == 1
     assert B._lib.nlinv_reconstruct(None, None, None, 1, 1, None, None, None) == 1
     assert B._lib.nlinv_plan_destroy(None) == 0
+    buf = ctypes.create_string_buffer(64)
+    assert B._lib.nlinv_plan_exchange_handle(None, buf) == 1
+    assert B._lib.nlinv_plan_connect(None, buf) == 1
+    assert B._lib.nlinv_plan_connect_local(None, None) == 1
 
 
 def test_nccl_unique_id():
