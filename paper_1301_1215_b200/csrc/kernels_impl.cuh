@@ -1040,7 +1040,8 @@ __device__ __forceinline__ void row_task(const RowArgs& a, int pair0, const floa
   const int g = threadIdx.x / T, t = threadIdx.x % T;
   const int pair = pair0 + g;
   const bool active = pair < a.J * n;
-  const int j = active ? pair / n : 0, yy = active ? pair % n : 0, row = q + yy;
+  const int pc = active ? pair : 0;   // an inactive group (tail of the last CTA) works on row 0 of coil 0
+  const int j = pc / n, yy = pc % n, row = q + yy;
   RowBuf buf{xbase + (size_t)g * L};
 
   if constexpr (MODE == RK_SETPOINT || MODE == RK_SETPOINT_FWD || MODE == RK_RSS) {
@@ -1079,7 +1080,7 @@ __device__ __forceinline__ void row_task(const RowArgs& a, int pair0, const floa
   // stores. A per-element "if (active)" makes the compiler put each load and its first use in one
   // branch region, which serialises the E load latencies.
   {
-    const float2* src = a.in + (active ? j * H + (size_t)yy * L : 0);
+    const float2* src = a.in + (size_t)j * H + (size_t)yy * L;
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = src[S::in_idx(t, psh_in<L>(e))];   // half-shifted input (psh_in)
   }
@@ -1746,6 +1747,37 @@ static cudaError_t launch_k234_l(const RowArgs& a, const float2* tw, cudaStream_
   }
 }
 
+// Force-load every kernel of this grid size (CUDA lazy loading loads a function at its first launch,
+// which can wait for the device to drain: with the peer-memory exchange a rank's kernel may spin on
+// a peer whose kernels the host has not enqueued yet, so nothing may be loaded lazily after that)
+template <int L>
+static cudaError_t preload_l() {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaSuccess;
+  auto get = [&](const void* f) { if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, f); };
+  get((const void*)col_kernel<L, CK_IFFT_W, false>);
+  get((const void*)col_kernel<L, CK_IFFT_W_CG, false>);
+  get((const void*)col_kernel<L, CK_FWDP, false>);
+  get((const void*)col_kernel<L, CK_FWDP, true>);
+  get((const void*)col_kernel<L, CK_PSF, false>);
+  get((const void*)col_kernel<L, CK_PSF, true>);
+  get((const void*)col_kernel<L, CK_RESADJ, false>);
+  get((const void*)col_kernel<L, CK_RESADJ, true>);
+  get((const void*)col_kernel<L, CK_ADJ1, false>);
+  get((const void*)col_kernel<L, CK_ADJ1, true>);
+  get((const void*)col_kernel<L, CK_FFT_W_NORMAL, false>);
+  get((const void*)col_kernel<L, CK_FFT_W_RHS, false>);
+  get((const void*)col_kernel<L, CK_FFT_W_ADJ, false>);
+  get((const void*)k5cg_kernel<L>);
+  get((const void*)row_kernel<L, RK_SETPOINT>);
+  get((const void*)row_kernel<L, RK_SETPOINT_FWD>);
+  get((const void*)row_kernel<L, RK_RSS>);
+  get((const void*)row_kernel<L, RK_K2>);
+  get((const void*)row_kernel<L, RK_K4>);
+  if constexpr (K234Geo<L>::kOk) get((const void*)k234_kernel<L>);
+  return e;
+}
+
 // ------------------------------------------------------------------ plain batched 2D transform
 // (debug / micro-benchmark entry: centred unitary F_c or F_c^H of `batch` images)
 template <int L, int DIR>
@@ -1843,7 +1875,8 @@ static cudaError_t launch_fft2d_l(const float2* in, float2* out, int batch, int 
   bool k5cg_fusable_##L(int J);                                                                  \
   bool k234_ok_##L();                                                                            \
   cudaError_t launch_k234_##L(const RowArgs& a, const float2* tw, cudaStream_t s);              \
-  int k234_max_clusters_##L();
+  int k234_max_clusters_##L();                                                                   \
+  cudaError_t preload_##L();
 #define NLV_INSTANTIATE(L)                                                                       \
   cudaError_t launch_col_##L(int mode, const ColArgs& a, const float2* tw, cudaStream_t s) {    \
     return launch_col_l<L>(mode, a, tw, s);                                                      \
@@ -1859,7 +1892,8 @@ static cudaError_t launch_fft2d_l(const float2* in, float2* out, int batch, int 
   bool k5cg_fusable_##L(int J) { return k5cg_fusable_l<L>(J); }                                  \
   bool k234_ok_##L() { return k234_ok_l<L>(); }                                                  \
   cudaError_t launch_k234_##L(const RowArgs& a, const float2* tw, cudaStream_t s) { return launch_k234_l<L>(a, tw, s); } \
-  int k234_max_clusters_##L() { return k234_max_clusters_l<L>(); }
+  int k234_max_clusters_##L() { return k234_max_clusters_l<L>(); }                                 \
+  cudaError_t preload_##L() { return preload_l<L>(); }
 
 #define NLV_FOR_EACH_NG(X) X(16) X(32) X(48) X(64) X(96) X(128) X(192) X(256) X(384) X(512) X(768) X(1024)
 NLV_FOR_EACH_NG(NLV_DECLARE)

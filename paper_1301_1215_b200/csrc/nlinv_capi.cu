@@ -524,7 +524,7 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
     // exercised and parity-tested on a single device)
     const char* fn = std::getenv("NLINV_FORCE_NCCL");
 #ifdef NLINV_WITH_NCCL
-    pl->multi = (prm.world > 1 && p->nccl_id != nullptr) || (prm.world == 1 && fn && fn[0] == '1');
+    pl->multi = (prm.world > 1 && prm.nccl_id != nullptr) || (prm.world == 1 && fn && fn[0] == '1');
 #else
     pl->multi = false;
     (void)fn;
@@ -607,6 +607,7 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
     }
     ok &= alloc((void**)&pl->xwin, xwin_bytes(pl->Q));
     ok &= alloc((void**)&pl->rss_sum, sizeof(float) * pl->Q);
+    ok &= preload_kernels(nx) == cudaSuccess;
   }
   ok &= alloc((void**)&pl->scal, sizeof(double) * SC_TOTAL);
   ok &= alloc((void**)&pl->partials, sizeof(double) * 8 * kMaxRedBlocks);
@@ -639,6 +640,7 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
   if (e == cudaSuccess) e = cudaMemset(pl->counter, 0, sizeof(unsigned) * 4);
   if (e == cudaSuccess && pl->kbar) e = cudaMemset(pl->kbar, 0, sizeof(unsigned) * 4);
   if (e == cudaSuccess && pl->xwin) e = cudaMemset(pl->xwin, 0, xwin_bytes(pl->Q));
+  if (e == cudaSuccess && pl->xwin) e = cudaDeviceSynchronize();   // zeroed flags before any peer looks
   if (e != cudaSuccess) {
     std::string msg = std::string("plan upload: ") + cudaGetErrorString(e);
     plan_free(pl);
@@ -816,6 +818,10 @@ nlinv_status enq_set_point(Enq& q, const float2* x, float2* fwd_out) {
   ra.in = pl->tA;
   ra.xrho = x;
   ra.out = fwd_out;
+  if (std::getenv("NLINV_DEBUG_PTRS"))
+    std::fprintf(stderr, "set_point: tA=%p tB=%p x=%p c_omega=%p rho_omega=%p slab=%p J=%d sizeof(RowArgs)=%zu\n",
+                 (void*)pl->tA, (void*)pl->tB, (const void*)x, (void*)pl->c_omega, (void*)pl->rho_omega, pl->slab, pl->J,
+                 sizeof(RowArgs));
   TRY(q.row(fwd_out ? RK_SETPOINT_FWD : RK_SETPOINT, ra));
   return NLINV_OK;
 }

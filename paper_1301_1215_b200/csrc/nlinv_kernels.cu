@@ -359,6 +359,22 @@ cudaError_t launch_k234(int ng, const RowArgs& a, const float2* tw, cudaStream_t
   return cudaErrorInvalidValue;
 }
 
+cudaError_t preload_kernels(int ng) {
+  cudaError_t e = cudaErrorInvalidValue;
+#define X(L) if (ng == L) e = preload_##L();
+  NLV_FOR_EACH_NG(X)
+#undef X
+  if (e != cudaSuccess) return e;
+  cudaFuncAttributes fa;
+  const void* fs[] = {(const void*)newton_update_kernel, (const void*)r_update_kernel, (const void*)image_kernel,
+                      (const void*)coil_sum_kernel, (const void*)rss_sum_kernel, (const void*)xchg_kernel,
+                      (const void*)init_x_kernel, (const void*)mask_count_kernel, (const void*)mask_scatter_kernel,
+                      (const void*)scatter_samples_kernel, (const void*)grid_radial_kernel};
+  for (const void* f : fs)
+    if ((e = cudaFuncGetAttributes(&fa, f)) != cudaSuccess) return e;
+  return cudaSuccess;
+}
+
 int k234_max_clusters(int ng) {
 #define X(L) if (ng == L) return k234_max_clusters_##L();
   NLV_FOR_EACH_NG(X)

@@ -175,6 +175,8 @@ bool k5cg_fusable(int ng, int J);
 bool k234_supported(int ng);
 cudaError_t launch_k234(int ng, const RowArgs& a, const float2* tw, cudaStream_t s);
 int k234_max_clusters(int ng);
+// load every kernel the plan may launch (no lazy loading once peers may spin on each other)
+cudaError_t preload_kernels(int ng);
 cudaError_t launch_coil_sum(int ng, const float2* S_all, int J, float2* S, cudaStream_t s);
 // generic two-phase peer exchange (one CTA): nsum scalars summed over ranks (slots src[i] -> dst[i] of
 // scal), nr0 scalars taken from rank 0, and optionally the RSS plane (rss_local [Q] of every rank summed

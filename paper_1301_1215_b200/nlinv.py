@@ -158,6 +158,7 @@ class Plan:
         first, count = c_int(), c_int()
         _check(_lib.nlinv_plan_local_coils(h, ctypes.byref(first), ctypes.byref(count)), h)
         self.first, self.count = first.value, count.value
+        self.rank, self.world = int(rank), int(world)
         self.n = ng // 2
 
     # ---------------------------------------------------------------- peer-memory exchange (world > 1, no NCCL id)
