@@ -148,12 +148,16 @@ def _run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_1301_1215_b200.dist import exchange_unique_id
-    nccl_id = exchange_unique_id(rank, world)
-
     from paper_1301_1215_b200 import radial_mask
+    from paper_1301_1215_b200.dist import connect_peers, exchange_unique_id
     mask0 = radial_mask(NG, SPOKES, TURNS, 0)
-    plan = Plan(NG, J, mask0, rank=rank, world=world, nccl_id=nccl_id)
+    if world > 1 and args.transport == "nccl":
+        plan = Plan(NG, J, mask0, rank=rank, world=world, nccl_id=exchange_unique_id(rank, world))
+    else:
+        # peer-memory exchange (default): every rank maps every rank's exchange window (CUDA IPC)
+        plan = Plan(NG, J, mask0, rank=rank, world=world)
+        if world > 1:
+            connect_peers(plan)
     frames, masks = make_frames(plan.first, plan.count)
     dframes = [torch.from_numpy(f).cuda() for f in frames]
     dmasks = [torch.from_numpy(m).cuda() for m in masks]
@@ -294,7 +298,8 @@ def _run_ours(args):
             "data": "synthetic (modified Shepp-Logan + Gaussian coil maps, rasterised radial spokes)",
             "config": {"workload": WORKLOAD, "ng": NG, "coils": J, "spokes": SPOKES, "turns": TURNS,
                        "newton_steps": NEWTON, "cg_iters": CG, "coils_per_rank": plan.count,
-                       "parallelism": f"coil-sharded x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"coil-sharded x{world} ({args.transport} exchange)" if world > 1
+                                       else "single GPU"),
                        "l2": "flushed (256 MB write) before every timed frame, outside the events",
                        "per_frame_ms": [round(m, 4) for m in ms_steps]},
             "e2e": {"value": round(args.steps / e2e_s, 3), "unit": "frames/s", "h2d_bytes_per_step": h2d,
@@ -406,6 +411,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="multi-GPU exchange: peer memory fused into the kernels (default) or NCCL all-reduces")
+    ap.add_argument("--dry-run", action="store_true", help="check the rank launch only (no GPU work)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world_env = os.environ.get("WORLD_SIZE")
@@ -413,6 +421,22 @@ def main():
         sys.exit(_relaunch(args))
     if world_env is not None and int(world_env) != args.gpus:
         sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}")
+    if args.dry_run:   # launcher check without a GPU: every rank reports over gloo, rank 0 prints
+        import torch.distributed as dist
+        world, rank, _ = _dist()
+        from paper_1301_1215_b200 import coil_partition
+        parts = [coil_partition(J, world, r) for r in range(world)]
+        if world > 1:
+            dist.init_process_group("gloo")
+            got = [None] * world
+            dist.all_gather_object(got, rank)
+            dist.destroy_process_group()
+        else:
+            got = [0]
+        if rank == 0:
+            print(json.dumps({"dry_run": True, "n_gpus": world, "ranks": got, "coils_per_rank": [c for _, c in parts],
+                              "transport": args.transport}))
+        return
     if args.impl == "reference":
         out = run_reference(args)
         if out is not None:

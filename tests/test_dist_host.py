@@ -73,3 +73,61 @@ def test_assemble_rejects_diverged_rho():
     b[0, 0, 0] = 1.0
     with pytest.raises(ValueError):
         D.assemble_unknowns([a, b], 3)
+
+
+def _ipc_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1301_1215_b200 import dist as D
+
+        class FakePlan:   # the two calls connect_peers makes on a peer-memory plan
+            def exchange_handle(self):
+                return bytes([rank]) * 64
+
+            def connect(self, handles):
+                self.handles = handles
+
+        fp = FakePlan()
+        D.connect_peers(fp)
+        q.put((rank, fp.handles))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_handle_exchange_rank_order():
+    """connect_peers all-gathers every rank's 64-byte exchange-window handle in rank order (the host
+    side of the peer-memory exchange, nlinv_plan_connect)."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert res[r] == [bytes([h]) * 64 for h in range(world)]
+
+
+def test_bench_launches_the_requested_ranks():
+    """`python bench.py --gpus 2` re-launches itself under torch.distributed.run with 2 ranks (dry run:
+    the ranks check in over gloo, no GPU work), and a WORLD_SIZE that contradicts --gpus is an error."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and sorted(line["ranks"]) == [0, 1] and line["coils_per_rank"] == [6, 6]
+    env2 = dict(env, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    bad = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=120, env=env2)
+    assert bad.returncode != 0 and "WORLD_SIZE" in bad.stderr
