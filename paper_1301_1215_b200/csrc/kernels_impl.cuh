@@ -314,6 +314,35 @@ __device__ __forceinline__ void tile_prefetch(float2* dst, const float2* img, in
   asm volatile("cp.async.commit_group;\n" ::);
 }
 
+// Column-tile prefetch with the tensor memory accelerator: the [L rows][CW columns] tile of coil j
+// of a [J][L][L] c64 array, described by a host-built CUtensorMap (3D: x, y, coil; 8-byte elements),
+// lands in shared memory as [row][CW] (the ColBuf layout) from ceil(L / 256) box loads issued by one
+// thread, completion tracked by an mbarrier (transaction bytes). Replaces L*CW/2 cp.async per CTA.
+__device__ __forceinline__ void tma_tile_issue(uint64_t* mbar, float2* dst, const void* tmap, int x0, int j, int L,
+                                               int CW) {
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb) : "memory");
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  const uint32_t bytes = (uint32_t)(L * CW * 8);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bytes) : "memory");
+  const int box = L <= 256 ? L : (L % 256 == 0 ? 256 : 192);   // box rows <= 256 (TMA limit)
+  for (int y0 = 0; y0 < L; y0 += box) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + (size_t)y0 * CW);
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+        ::"r"(d), "l"(tmap), "r"(x0), "r"(y0), "r"(j), "r"(mb) : "memory");
+  }
+}
+__device__ __forceinline__ void tma_tile_wait(uint64_t* mbar) {
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done) : "r"(mb) : "memory");
+  }
+}
+
 // debug timeline of one CTA (globaltimer ns), compiled in with -DNLV_TRACE
 __device__ __forceinline__ void trace_stamp(unsigned long long* tr, int k) {
 #ifdef NLV_TRACE
@@ -715,8 +744,13 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   // r (dx in the last iteration) was written by the previous CG iteration's pass, which completed
   // before the passes in between could run: the L2-only (cp.async.cg) prefetch is issued before
   // griddepcontrol.wait and overlaps the drain of the previous pass
-  bool pf_on = false;
-  if (!last) {
+  bool pf_on = false, pf_tma = false;
+  __shared__ alignas(8) uint64_t pf_bar;
+  const void* tmap = last ? a.tmap_dx : a.tmap_r;
+  if (tmap != nullptr && (!last || hasdx)) {   // TMA (UTMALDG): one thread issues the tile loads
+    if (tid == 0) tma_tile_issue(&pf_bar, pf, tmap, tile * CW, j, L, CW);
+    pf_tma = true;
+  } else if (!last) {
     tile_prefetch<L, CW>(pf, a.r + j * N, tile * CW);
     pf_on = true;
   } else if (hasdx) {
@@ -811,6 +845,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   fft<L, -1, omega_in_zmask<L>()>(v, t, tw, buf, SyncBlock{});   // T4: Omega rows only
   trace_stamp(a.trace, 2);
   if (pf_on) prefetch_wait();   // the r / dx tile is complete (all threads' copies)
+  if (pf_tma) tma_tile_wait(&pf_bar);
 
   // epilogue: A p_chat = w^-1 (-1)^k . + alpha p; p parked in the (now free) exchange buffer
   {
@@ -1014,7 +1049,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
 template <int L>
 __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) k5cg_kernel(ColArgs a, const float2* __restrict__ twg) {
   constexpr int CW = ColGeo<L>::CW;
-  extern __shared__ float4 smem_raw[];
+  extern __shared__ __align__(128) float4 smem_raw[];   // pf (TMA destination) is 128-byte aligned
   float2* tw = reinterpret_cast<float2*>(smem_raw);
   float2* xb = tw + L;
   double* red = reinterpret_cast<double*>(xb + (size_t)L * CW);   // 128 doubles

@@ -4,6 +4,8 @@
 // IRGNM / CG iteration of PAPER.md Eq. 3 by enqueuing the kernels of
 // nlinv_kernels.cu. No arithmetic of the method runs here except the one-time tables
 // (twiddles, w^{-1}) and the integer radial rasteriser, which are host setup.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -70,6 +72,7 @@ struct nlinv_plan_s {
   bool k234 = false;                      // cluster-fused K2 -> K3 -> K4 in the fused CG loop (k234_kernel)
   bool cg1 = false;                       // unfused CG: one (grouped) scalar all-reduce per iteration (R19)
   unsigned* kbar = nullptr;               // its grid barrier
+  CUtensorMap* tmaps = nullptr;           // device copies of the TMA tensor maps of r and dx (k5cg prefetch)
   double* kpart = nullptr;                // its dot partials
   unsigned long long* trace = nullptr;
   double *scal = nullptr, *partials = nullptr;
@@ -467,7 +470,7 @@ static void plan_free(nlinv_plan pl) {
   }
   void* ptrs[] = {pl->tw, pl->winv, pl->mask, pl->xref, pl->dx, pl->r, pl->p, pl->Ap, pl->tA, pl->tB,
                   pl->c_omega, pl->rho_omega, pl->S_all, pl->S, pl->S_sum, pl->rss_all, pl->rss, pl->rss_sum,
-                  pl->kbar, pl->kpart, pl->scal, pl->partials,
+                  pl->kbar, pl->kpart, pl->tmaps, pl->scal, pl->partials,
                   pl->counter, pl->h_frame, pl->h_x, pl->h_img, pl->midx, pl->mcount, pl->mnnz, pl->h_samples};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -480,6 +483,35 @@ static void plan_free(nlinv_plan pl) {
   if (pl->comm) ncclCommDestroy(pl->comm);
 #endif
   delete pl;
+}
+
+// TMA descriptors of the chat blocks [J][ng][ng] (8-byte elements) of r and dx: box = one fused-pass
+// column tile (CW columns) x up to 256 rows x one coil. false if the driver entry point is missing.
+static bool make_tile_maps(int ng, int J, float2* r_chat, float2* dx_chat, CUtensorMap out[2]) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      cudaGetLastError();
+      return false;
+    }
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const int cw = ng / col_tiles(ng);
+  const cuuint64_t dims[3] = {(cuuint64_t)ng, (cuuint64_t)ng, (cuuint64_t)J};
+  const cuuint64_t strides[2] = {(cuuint64_t)ng * 8, (cuuint64_t)ng * ng * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)cw, (cuuint32_t)(ng <= 256 ? ng : (ng % 256 == 0 ? 256 : 192)), 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  float2* bases[2] = {r_chat, dx_chat};
+  for (int k = 0; k < 2; ++k) {
+    if (enc(&out[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, bases[k], dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  return true;
 }
 
 extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint8_t* mask, const nlinv_params* p,
@@ -597,6 +629,15 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
     if (pl->fused) {
       ok &= alloc((void**)&pl->kbar, sizeof(unsigned) * 4);
       ok &= alloc((void**)&pl->kpart, sizeof(double) * 8 * kMaxRedBlocks);
+      // TMA tile prefetch of r / dx in the fused pass (NLINV_TMA=0: cp.async instead)
+      const char* tm = std::getenv("NLINV_TMA");
+      if (ok && !(tm && tm[0] == '0')) {
+        CUtensorMap h[2];
+        if (make_tile_maps(nx, pl->J, pl->r + N, pl->dx + N, h)) {
+          ok &= alloc((void**)&pl->tmaps, sizeof(h));
+          ok &= ok && cudaMemcpy(pl->tmaps, h, sizeof(h), cudaMemcpyHostToDevice) == cudaSuccess;
+        }
+      }
     }
   }
   if (pl->p2p) {
@@ -1043,6 +1084,10 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
         c5.x_rho = x;
         c5.bar_count = pl->kbar;
         c5.fpart = pl->kpart;
+        if (pl->tmaps) {
+          c5.tmap_r = pl->tmaps;
+          c5.tmap_dx = pl->tmaps + 1;
+        }
         TRY(q.col(CK_K5CG, c5));
       }
       continue;

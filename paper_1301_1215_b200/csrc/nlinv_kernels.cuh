@@ -114,6 +114,8 @@ struct ColArgs {
   float alpha;
   int J;
   XPeers xp;               // peer-memory exchange (world > 1 without NCCL); xp.G == 0: off
+  const void* tmap_r;      // k5cg: CUtensorMap (device, 64-B aligned) of the chat blocks of r / dx for the TMA
+  const void* tmap_dx;     // tile prefetch; nullptr: cp.async prefetch
 };
 
 struct RowArgs {
