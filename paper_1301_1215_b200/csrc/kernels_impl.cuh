@@ -358,7 +358,9 @@ __device__ __forceinline__ void trace_stamp(unsigned long long* tr, int k) {
 // Returns this thread's contributions to the (rho, chat) reductions of MODE. The caller owns
 // the twiddle table tw (shared) and the exchange buffer xb (shared, L*CW float2). Every thread
 // of the CTA must call it (the transform uses __syncthreads).
-template <int L, int MODE, bool PW = false>   // PW: real-valued P_k (KB gridding, R22), a separate instantiation
+// PW: real-valued P_k (KB gridding, R22); XP: peer-memory exchange (world > 1) -- separate instantiations,
+// so the single-GPU kernels carry none of that code
+template <int L, int MODE, bool PW = false, bool XP = false>
 __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, const float2* tw, float2* xb,
                                          double& acc_rho, double& acc, double* acc3, int rlo = 0, int rhi = L,
                                          bool tw_async = false, const uint32_t* pre_mbits = nullptr) {
@@ -400,7 +402,7 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
           float2 sv = make_float2(0.f, 0.f);
           if (xx >= q && xx < q + n && y >= q && y < q + n) {
             const size_t o = (size_t)(y - q) * n + (xx - q);
-            if (a.xp.G > 0) sv = x_sum_S(a.xp, x_epoch(a.xp, XK_S), Qs, o);   // ranks' planes, rank order
+            if constexpr (XP) sv = x_sum_S(*a.xp, x_epoch(*a.xp, XK_S), Qs, o);   // ranks' planes, rank order
             else for (int sp = 0; sp < a.nS; ++sp) sv = cadd(sv, a.S[sp * Qs + o]);
           }
           if constexpr (MODE == CK_FFT_W_NORMAL) {
@@ -651,7 +653,7 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
   }
 }
 
-template <int L, int MODE, bool PW = false>   // PW: real-valued P_k (KB gridding, R22) -- its own kernel
+template <int L, int MODE, bool PW = false, bool XP = false>   // PW, XP: see col_task
 #ifndef NLV_MINB
 #define NLV_MINB 2  // <= 128 registers: two 256-thread CTAs per SM (more registers halve residency)
 #endif
@@ -674,11 +676,10 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColAr
   }
   pdl_wait();
   pdl_trigger();
-  if constexpr (MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ) {
-    if (a.xp.G > 0) {   // peer exchange: every rank's K4 has published its coil-sum plane
-      if (threadIdx.x == 0) x_wait_all(a.xp, XK_S, x_epoch(a.xp, XK_S));
-      __syncthreads();
-    }
+  if constexpr (XP && (MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ)) {
+    // peer exchange: every rank's K4 has published its coil-sum plane
+    if (threadIdx.x == 0) x_wait_all(*a.xp, XK_S, x_epoch(*a.xp, XK_S));
+    __syncthreads();
   }
   if constexpr (MODE == CK_IFFT_W_CG) {
     if (a.cg1) {
@@ -692,7 +693,7 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColAr
   double acc_rho = 0.0, acc = 0.0;
   const int j = (int)blockIdx.y;
   double acc3[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};   // single-reduction CG dots (rho: 0-2, chat: 3-5)
-  col_task<L, MODE, PW>(a, blockIdx.x, j, tw, xb, acc_rho, acc, acc3, 0, L, true, MODE == CK_PSF ? &mb : nullptr);
+  col_task<L, MODE, PW, XP>(a, blockIdx.x, j, tw, xb, acc_rho, acc, acc3, 0, L, true, MODE == CK_PSF ? &mb : nullptr);
   trace_stamp(a.trace, 5);
   if constexpr (MODE == CK_RESADJ || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_NORMAL) {
     if (MODE == CK_FFT_W_NORMAL && a.cg1 && a.partials != nullptr) {
@@ -725,7 +726,7 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColAr
 // must be the directly computed one: feeding the expanded value back into the next expansion
 // accumulates its absolute error and ruins late iterations (measured in an fp32 model: 5e-2 on
 // the C1 image vs 6e-5 with the direct <r_i,r_i>).
-template <int L>
+template <int L, bool XP>
 __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, float2* xb, float2* pf, double* red) {
   using C = Cfg<L>;
   using S = Sched<L>;
@@ -761,10 +762,10 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   pdl_trigger();
   // peer exchange: wait for every rank's coil-sum plane of this iteration (published by its K4)
   unsigned long long eS = 0, eD = 0;
-  if (a.xp.G > 0) {
-    eS = x_epoch(a.xp, XK_S);
-    eD = x_epoch(a.xp, XK_DOTS) + 1;   // read before CTA 0 publishes it (after the grid barrier)
-    if (tid == 0) x_wait_all(a.xp, XK_S, eS);
+  if constexpr (XP) {
+    eS = x_epoch(*a.xp, XK_S);
+    eD = x_epoch(*a.xp, XK_DOTS) + 1;   // read before CTA 0 publishes it (after the grid barrier)
+    if (tid == 0) x_wait_all(*a.xp, XK_S, eS);
     __syncthreads();
   }
 
@@ -798,7 +799,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
     float2 sv = make_float2(0.f, 0.f);
     if (xx >= q && xx < q + n && y >= q && y < q + n) {
       const size_t o = (size_t)(y - q) * n + (xx - q);
-      if (a.xp.G > 0) sv = x_sum_S(a.xp, eS, Qs, o);   // the ranks' coil-sum planes, rank order
+      if constexpr (XP) sv = x_sum_S(*a.xp, eS, Qs, o);   // the ranks' coil-sum planes, rank order
       else for (int s2 = 0; s2 < a.nS; ++s2) sv = cadd(sv, a.S[s2 * Qs + o]);
     }
     return sv;
@@ -810,7 +811,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
       const size_t i = lo + tid + (size_t)u * blockDim.x;
       const bool ok = i < hi;
       sp[u] = ok ? a.rho_a[i] : make_float2(0.f, 0.f);
-      sr[u] = ok ? a.rho_r[i] : make_float2(0.f, 0.f);
+      sr[u] = (ok && !last) ? a.rho_r[i] : make_float2(0.f, 0.f);
       sv[u] = ok ? stripe_sum(i) : make_float2(0.f, 0.f);
     }
 #pragma unroll
@@ -830,9 +831,9 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
       const float2 o = make_float2(fmaf(a.alpha, pv.x, sv.x), fmaf(a.alpha, pv.y, sv.y));
       a.rho_out[i] = o;
       d[0] += (double)pv.x * o.x + (double)pv.y * o.y;
-      const float2 rv = a.rho_r[i];
-      d[6] += (double)rv.x * rv.x + (double)rv.y * rv.y;
       if (!last) {
+        const float2 rv = a.rho_r[i];
+        d[6] += (double)rv.x * rv.x + (double)rv.y * rv.y;
         d[2] += (double)rv.x * o.x + (double)rv.y * o.y;
         d[4] += (double)o.x * o.x + (double)o.y * o.y;
       }
@@ -868,10 +869,11 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
         v[e0 + u] = o;
         buf(k) = pv[u];
         d[1] += (double)pv[u].x * o.x + (double)pv[u].y * o.y;
-        // <r_i, r_i> directly from the stored r_i in every iteration (R19); the last one reads r here
-        const float2 rv = last ? a.r[j * N + (size_t)k * L + x] : pf[k * CW + c];
-        d[7] += (double)rv.x * rv.x + (double)rv.y * rv.y;
+        // <r_i, r_i> directly from the stored r_i (R19); the last iteration takes the previous
+        // pass's partials of the r_i it wrote (rr_next below) instead of reading r again
         if (!last) {
+          const float2 rv = pf[k * CW + c];
+          d[7] += (double)rv.x * rv.x + (double)rv.y * rv.y;
           d[3] += (double)rv.x * o.x + (double)rv.y * o.y;
           d[5] += (double)o.x * o.x + (double)o.y * o.y;
         }
@@ -907,26 +909,52 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
       if (lane == 0) red[k] = sk;
     }
     __syncthreads();
+    if (last) {
+      // <r_{L-1}, r_{L-1}> of the stored r: summed by the previous fused pass as it wrote r (per-CTA
+      // partials in fpart[8 nb ..], same CTA grid, fixed order), or the rhs pass's <b, b> when L = 1
+      if (w == 0) {
+        double sr = 0.0, sc = 0.0;
+        if (a.iter > 0) {
+          for (unsigned b = lane; b < nb; b += 32) {
+            sr += __ldcg(a.fpart + 8 * nb + b);
+            sc += __ldcg(a.fpart + 9 * nb + b);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            sr += __shfl_xor_sync(0xffffffffu, sr, o);
+            sc += __shfl_xor_sync(0xffffffffu, sc, o);
+          }
+        } else {
+          sr = a.scal[SC_RR_RHO];
+          sc = a.scal[SC_RR_CHAT];
+        }
+        if (lane == 0) {
+          red[6] = sr;
+          red[7] = sc;
+        }
+      }
+      __syncthreads();
+    }
   }
-  if (a.xp.G > 0) {
+  if constexpr (XP) {
     // peer exchange of the dots (one epoch of kind XK_DOTS): CTA 0 publishes this rank's totals; every
     // CTA waits for all ranks and forms the global totals in the same order on every rank: the chat
     // parts summed over ranks (ascending), the replicated rho parts taken from rank 0, so gamma and
     // beta -- and with them the rho replicas -- are bit-identical on all ranks
     if (bid == 0 && tid == 0) {
-      double* dd = xw_dots(a.xp.win[a.xp.rank], (int)(eD & 1ull));
+      double* dd = xw_dots(a.xp->win[a.xp->rank], (int)(eD & 1ull));
       for (int k = 0; k < NV; ++k) dd[k] = red[k];
-      x_publish(a.xp, XK_DOTS, eD);
+      x_publish(*a.xp, XK_DOTS, eD);
     }
-    if (tid == 0) x_wait_all(a.xp, XK_DOTS, eD);
+    if (tid == 0) x_wait_all(*a.xp, XK_DOTS, eD);
     __syncthreads();
     double gk = 0.0;
     if (tid < NV) {
       const int par = (int)(eD & 1ull);
       if ((tid & 1) == 0) {
-        gk = __ldcv(xw_dots(a.xp.win[0], par) + tid);
+        gk = __ldcv(xw_dots(a.xp->win[0], par) + tid);
       } else {
-        for (int h = 0; h < a.xp.G; ++h) gk += __ldcv(xw_dots(a.xp.win[h], par) + tid);
+        for (int h = 0; h < a.xp->G; ++h) gk += __ldcv(xw_dots(a.xp->win[h], par) + tid);
       }
     }
     __syncthreads();
@@ -989,7 +1017,8 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   }
 
   // r_{i+1} = r - gamma Ap; dx += gamma p; p_{i+1} = r_{i+1} + beta p (in place); t = w^-1 p_{i+1}
-  // (K1 prologue)
+  // (K1 prologue). <r_{i+1}, r_{i+1}> partials of the stored r_{i+1} for the last iteration (rr_next)
+  double rrn_r = 0.0, rrn_c = 0.0;
   {
     constexpr int CH = 8;
 #pragma unroll
@@ -1009,6 +1038,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
         const float2 rv = pf[k * CW + c], pv = buf(k);
         const float2 rn = make_float2(fmaf(-gamma, v[e0 + u].x, rv.x), fmaf(-gamma, v[e0 + u].y, rv.y));
         a.r[i] = rn;
+        rrn_c += (double)rn.x * rn.x + (double)rn.y * rn.y;
         a.dx[i] = make_float2(fmaf(gamma, pv.x, dv[u].x), fmaf(gamma, pv.y, dv[u].y));
         const float2 pn = make_float2(fmaf(beta, pv.x, rn.x), fmaf(beta, pv.y, rn.y));
         a.p[i] = pn;
@@ -1020,6 +1050,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   auto update_rho = [&](size_t i, float2 av, float2 rv, float2 pv) {
     const float2 rn = make_float2(fmaf(-gamma, av.x, rv.x), fmaf(-gamma, av.y, rv.y));
     a.rho_r[i] = rn;
+    rrn_r += (double)rn.x * rn.x + (double)rn.y * rn.y;
     const float2 dv = hasdx ? a.rho_dx[i] : make_float2(0.f, 0.f);
     a.rho_dx[i] = make_float2(fmaf(gamma, pv.x, dv.x), fmaf(gamma, pv.y, dv.y));
     a.rho_p[i] = make_float2(fmaf(beta, pv.x, rn.x), fmaf(beta, pv.y, rn.y));
@@ -1034,6 +1065,28 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
     for (size_t i = lo + tid; i < hi; i += blockDim.x) update_rho(i, a.rho_out[i], a.rho_r[i], a.rho_a[i]);
   }
   trace_stamp(a.trace, 4);
+  {  // <r_{i+1}, r_{i+1}> partials of this CTA (warp trees, warps in order) for the next pass
+    const int w = tid >> 5, lane = tid & 31, nw = (int)(blockDim.x >> 5);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      rrn_r += __shfl_xor_sync(0xffffffffu, rrn_r, o);
+      rrn_c += __shfl_xor_sync(0xffffffffu, rrn_c, o);
+    }
+    if (lane == 0) {
+      red[8 + 2 * w] = rrn_r;
+      red[9 + 2 * w] = rrn_c;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double sr = 0.0, sc = 0.0;
+      for (int ww = 0; ww < nw; ++ww) {
+        sr += red[8 + 2 * ww];
+        sc += red[9 + 2 * ww];
+      }
+      a.fpart[8 * nb + bid] = sr;
+      a.fpart[9 * nb + bid] = sc;
+    }
+  }
   __syncthreads();   // every parked p has been read: xb becomes the exchange buffer again
   out_to_in<L>(v, t, buf, SyncBlock{});
   fft<L, +1>(v, t, tw, buf, SyncBlock{});
@@ -1046,7 +1099,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   }
 }
 
-template <int L>
+template <int L, bool XP>
 __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) k5cg_kernel(ColArgs a, const float2* __restrict__ twg) {
   constexpr int CW = ColGeo<L>::CW;
   extern __shared__ __align__(128) float4 smem_raw[];   // pf (TMA destination) is 128-byte aligned
@@ -1056,7 +1109,7 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) k5cg_kernel(ColA
   float2* pf = reinterpret_cast<float2*>(red + 128);
   trace_stamp(a.trace, 0);
   tw_copy_async(tw, twg, L);
-  k5cg_task<L>(a, tw, xb, pf, red);   // griddepcontrol.wait inside, after the r prefetch
+  k5cg_task<L, XP>(a, tw, xb, pf, red);   // griddepcontrol.wait inside, after the r prefetch
 }
 
 // ------------------------------------------------------------------ row task (one (coil, Omega row) per group)
@@ -1344,7 +1397,7 @@ struct RowGeo {
   static constexpr size_t SMEM_K2 = sizeof(float2) * ((size_t)L * (GPC + 1) + (size_t)GPC * 3 * (L / 2));
 };
 
-template <int L, int MODE>
+template <int L, int MODE, bool XP = false>   // XP: K4 with the peer-memory exchange (its own instantiation)
 __global__ void __launch_bounds__(256, NLV_MINB) row_kernel(RowArgs a, const float2* __restrict__ twg) {
   extern __shared__ float4 smem_raw[];
   float2* tw = reinterpret_cast<float2*>(smem_raw);
@@ -1354,13 +1407,13 @@ __global__ void __launch_bounds__(256, NLV_MINB) row_kernel(RowArgs a, const flo
     // CTA = (Omega row, chunk of a.kchunk coils); chunk c writes coil-sum plane c. rho|Omega and
     // c_j|Omega (fixed for the Newton step) are read before griddepcontrol.wait
     const int jlo = blockIdx.y * a.kchunk, jhi = min(a.J, jlo + a.kchunk);
-    if (a.xp.G > 0) {
+    if constexpr (XP) {
       // peer exchange: the rank's coil-sum plane (one chunk = all local coils) goes straight into
       // the exchange window's buffer of the next epoch; the last CTA publishes it
       RowArgs b = a;
-      b.S = xw_S(a.xp.win[a.xp.rank], (int)((x_epoch(a.xp, XK_S) + 1) & 1ull), (size_t)(L / 2) * (L / 2));
+      b.S = xw_S(a.xp->win[a.xp->rank], (int)((x_epoch(*a.xp, XK_S) + 1) & 1ull), (size_t)(L / 2) * (L / 2));
       row_task_k4<L>(b, blockIdx.x, jlo, jhi, 0, tw, xb, xb + (size_t)L * (blockDim.x / Cfg<L>::T), true, true);
-      x_publish_last_block(a.xp, XK_S);
+      x_publish_last_block(*a.xp, XK_S);
     } else {
       row_task_k4<L>(a, blockIdx.x, jlo, jhi, blockIdx.y, tw, xb, xb + (size_t)L * (blockDim.x / Cfg<L>::T), true, true);
     }
@@ -1629,8 +1682,10 @@ static cudaError_t launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, si
 template <int L>
 static bool k5cg_fusable_l(int J) {
   if (ColGeo<L>::THREADS < 64) return false;
-  auto kern = k5cg_kernel<L>;
+  auto kern = k5cg_kernel<L, false>;
   const size_t smem = ColGeo<L>::SMEM_PF;
+  if (cudaFuncSetAttribute(k5cg_kernel<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return false;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return false;
   int dev = 0, nsm = 0, per = 0;
   cudaGetDevice(&dev);
@@ -1641,7 +1696,7 @@ static bool k5cg_fusable_l(int J) {
 
 template <int L>
 static cudaError_t launch_k5cg_t(const ColArgs& a, const float2* tw, cudaStream_t s) {
-  auto kern = k5cg_kernel<L>;
+  auto kern = a.xp != nullptr ? k5cg_kernel<L, true> : k5cg_kernel<L, false>;
   const size_t smem = ColGeo<L>::SMEM_PF;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -1651,7 +1706,10 @@ static cudaError_t launch_k5cg_t(const ColArgs& a, const float2* tw, cudaStream_
 template <int L, int MODE>
 static cudaError_t launch_col_t(const ColArgs& a, const float2* tw, cudaStream_t s) {
   constexpr bool kPWable = (MODE == CK_PSF || MODE == CK_RESADJ || MODE == CK_FWDP || MODE == CK_ADJ1);
-  auto kern = (kPWable && a.pw != nullptr) ? col_kernel<L, MODE, kPWable> : col_kernel<L, MODE, false>;
+  constexpr bool kXPable = (MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ);
+  auto kern = (kPWable && a.pw != nullptr) ? col_kernel<L, MODE, kPWable>
+              : (kXPable && a.xp != nullptr) ? col_kernel<L, MODE, false, kXPable>
+                                           : col_kernel<L, MODE, false>;
   const size_t smem = ColGeo<L>::SMEM;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -1679,7 +1737,7 @@ static cudaError_t launch_col_l(int mode, const ColArgs& a, const float2* tw, cu
 template <int L, int MODE>
 static cudaError_t launch_row_t(const RowArgs& a0, const float2* tw, cudaStream_t s) {
   const size_t smem = RowGeo<L>::SMEM;
-  auto kern = row_kernel<L, MODE>;
+  auto kern = (MODE == RK_K4 && a0.xp != nullptr) ? row_kernel<L, MODE, MODE == RK_K4> : row_kernel<L, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if constexpr (MODE == RK_K4) {
@@ -1803,7 +1861,12 @@ static cudaError_t preload_l() {
   get((const void*)col_kernel<L, CK_FFT_W_NORMAL, false>);
   get((const void*)col_kernel<L, CK_FFT_W_RHS, false>);
   get((const void*)col_kernel<L, CK_FFT_W_ADJ, false>);
-  get((const void*)k5cg_kernel<L>);
+  get((const void*)k5cg_kernel<L, false>);
+  get((const void*)k5cg_kernel<L, true>);
+  get((const void*)col_kernel<L, CK_FFT_W_NORMAL, false, true>);
+  get((const void*)col_kernel<L, CK_FFT_W_RHS, false, true>);
+  get((const void*)col_kernel<L, CK_FFT_W_ADJ, false, true>);
+  get((const void*)row_kernel<L, RK_K4, true>);
   get((const void*)row_kernel<L, RK_SETPOINT>);
   get((const void*)row_kernel<L, RK_SETPOINT_FWD>);
   get((const void*)row_kernel<L, RK_RSS>);

@@ -66,6 +66,7 @@ struct nlinv_plan_s {
   bool multi = false;                     // NCCL collective code path (world > 1 with an NCCL id, or NLINV_FORCE_NCCL=1)
   bool p2p = false;                       // peer-memory exchange (world > 1 without an NCCL id)
   XPeers xp{};                            // connected peers (xp.G == 0 until nlinv_plan_connect*)
+  XPeers* xp_dev = nullptr;               // device copy of xp passed to the kernels (nullptr until connected)
   char* xwin = nullptr;                   // this rank's exchange window (IPC-exportable)
   std::vector<void*> ipc_open;            // peer windows opened through CUDA IPC
   bool fused = false;                     // fused K5 + CG + K1 pass, one grid barrier (k5cg_kernel, R19)
@@ -470,7 +471,7 @@ static void plan_free(nlinv_plan pl) {
   }
   void* ptrs[] = {pl->tw, pl->winv, pl->mask, pl->xref, pl->dx, pl->r, pl->p, pl->Ap, pl->tA, pl->tB,
                   pl->c_omega, pl->rho_omega, pl->S_all, pl->S, pl->S_sum, pl->rss_all, pl->rss, pl->rss_sum,
-                  pl->kbar, pl->kpart, pl->tmaps, pl->scal, pl->partials,
+                  pl->kbar, pl->kpart, pl->tmaps, pl->xp_dev, pl->scal, pl->partials,
                   pl->counter, pl->h_frame, pl->h_x, pl->h_img, pl->midx, pl->mcount, pl->mnnz, pl->h_samples};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -628,7 +629,7 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
     pl->k234 = pl->fused && (kc && kc[0] == '1') && k234_supported(nx);
     if (pl->fused) {
       ok &= alloc((void**)&pl->kbar, sizeof(unsigned) * 4);
-      ok &= alloc((void**)&pl->kpart, sizeof(double) * 8 * kMaxRedBlocks);
+      ok &= alloc((void**)&pl->kpart, sizeof(double) * 10 * kMaxRedBlocks);   // 8 dots + 2 <r_{i+1},r_{i+1}>
       // TMA tile prefetch of r / dx in the fused pass (NLINV_TMA=0: cp.async instead)
       const char* tm = std::getenv("NLINV_TMA");
       if (ok && !(tm && tm[0] == '0')) {
@@ -784,7 +785,7 @@ struct Enq {
     a.scal_w = pl->scal;
     a.counter = pl->counter;
     a.J = pl->J;
-    a.xp = pl->xp;
+    a.xp = pl->xp_dev;
     const char* name = kColNames[mode];
     if (mode == CK_FFT_W_RHS && a.fuse_k1) name = "col_rhs_k1";
     if (mode == CK_K5CG) name = a.fuse_k1 ? "col_k5_cg_k1" : "col_k5_newton";
@@ -792,7 +793,7 @@ struct Enq {
   }
   nlinv_status row(int mode, RowArgs a) {
     a.J = pl->J;
-    if (mode == RK_K4) a.xp = pl->xp;
+    if (mode == RK_K4) a.xp = pl->xp_dev;
     a.c_omega = pl->c_omega;
     a.rho_omega = pl->rho_omega;
     return kern(kRowNames[mode], [&] { return launch_row(pl->ng, mode, a, pl->tw, s); });
@@ -1565,6 +1566,8 @@ extern "C" nlinv_status nlinv_plan_exchange_handle(nlinv_plan pl, unsigned char 
 static nlinv_status connect_done(nlinv_plan pl) {
   pl->xp.G = pl->world;
   pl->xp.rank = pl->rank;
+  if (!pl->xp_dev) CU(cudaMalloc((void**)&pl->xp_dev, sizeof(XPeers)));
+  CU(cudaMemcpy(pl->xp_dev, &pl->xp, sizeof(XPeers), cudaMemcpyHostToDevice));
   if (pl->gexec) {   // a graph captured before the peers were known is stale
     cudaGraphExecDestroy(pl->gexec);
     pl->gexec = nullptr;

@@ -113,7 +113,7 @@ struct ColArgs {
                            // K1 applies r -= gamma Ap (A p from src2 / rho_a) before the p update
   float alpha;
   int J;
-  XPeers xp;               // peer-memory exchange (world > 1 without NCCL); xp.G == 0: off
+  const XPeers* xp;        // peer-memory exchange (world > 1 without NCCL): device copy; nullptr: off
   const void* tmap_r;      // k5cg: CUtensorMap (device, 64-B aligned) of the chat blocks of r / dx for the TMA
   const void* tmap_dx;     // tile prefetch; nullptr: cp.async prefetch
 };
@@ -129,7 +129,7 @@ struct RowArgs {
   float* rss;              // [J][n][n] per-coil |c_j|^2 (RSS)
   const uint8_t* mask;     // [ng][ng] P_k (cluster-fused K2-K3-K4)
   int J;
-  XPeers xp;               // peer-memory exchange: K4 writes its coil-sum plane into the window and publishes
+  const XPeers* xp;        // peer-memory exchange: K4 writes its coil-sum plane into the window and publishes
   int kchunk;              // K4 coils per CTA (set by the launcher)
 };
 int k4_planes(int ng, int J);  // number of K4 coil-sum planes
