@@ -903,7 +903,15 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
     // totals: warp w sums value k = w (+ nw ...) over all CTAs in a fixed order -> identical in every CTA
     for (int k = w; k < NV; k += nw) {
       double sk = 0.0;
-      for (unsigned b = lane; b < nb; b += 32) sk += __ldcg(a.fpart + k * nb + b);
+      // the partials of 8 CTAs per lane are loaded together (independent L2 loads in flight), then
+      // added in ascending CTA order, the same order in every CTA
+      for (unsigned b0 = lane; b0 < nb; b0 += 256) {
+        double tk[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) tk[u] = (b0 + 32u * u < nb) ? __ldcg(a.fpart + k * nb + b0 + 32u * u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sk += tk[u];
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) sk += __shfl_xor_sync(0xffffffffu, sk, o);
       if (lane == 0) red[k] = sk;
@@ -915,9 +923,19 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
       if (w == 0) {
         double sr = 0.0, sc = 0.0;
         if (a.iter > 0) {
-          for (unsigned b = lane; b < nb; b += 32) {
-            sr += __ldcg(a.fpart + 8 * nb + b);
-            sc += __ldcg(a.fpart + 9 * nb + b);
+          for (unsigned b0 = lane; b0 < nb; b0 += 256) {
+            double tr[8], tc[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const bool ok = b0 + 32u * u < nb;
+              tr[u] = ok ? __ldcg(a.fpart + 8 * nb + b0 + 32u * u) : 0.0;
+              tc[u] = ok ? __ldcg(a.fpart + 9 * nb + b0 + 32u * u) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              sr += tr[u];
+              sc += tc[u];
+            }
           }
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) {
