@@ -248,6 +248,11 @@ nlinv_status nlinv_plan_connect_local(nlinv_plan plan, const nlinv_plan* plans);
  * (cudaOccupancyMaxActiveClusters); < 0 if that pass is not built for ng. Needs a device. */
 int nlinv_debug_k234_clusters(int ng);
 
+/* Micro-benchmark entry (the paper's axpy of Fig. 4): y = a x + y over n
+ * floats (device pointers, n a multiple of 4, 16-byte aligned), enqueued on `stream`. ERR_ARG on NULL
+ * pointers or a bad n. No plan needed. */
+nlinv_status nlinv_debug_axpy(float a, const float* x, float* y, long long n, void* stream);
+
 /* Number of kernels this library enqueued since plan creation (launch-count evidence). */
 long long nlinv_plan_launch_count(nlinv_plan plan);
 

@@ -1614,3 +1614,10 @@ extern "C" nlinv_status nlinv_plan_connect_local(nlinv_plan pl, const nlinv_plan
   }
   return connect_done(pl);
 }
+
+extern "C" nlinv_status nlinv_debug_axpy(float a, const float* x, float* y, long long n, void* stream) {
+  nlinv_plan pl = nullptr;
+  if (!x || !y || n < 0 || n % 4) return fail(pl, NLINV_ERR_ARG, "axpy: NULL pointer or n not a multiple of 4");
+  CU(launch_axpy(a, x, y, n, (cudaStream_t)stream));
+  return NLINV_OK;
+}

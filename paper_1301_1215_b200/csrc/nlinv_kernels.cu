@@ -138,6 +138,29 @@ cudaError_t launch_xchg(const XchgArgs& a, cudaStream_t s) {
   return launch_k(xchg_kernel, dim3(1), dim3(1024), 0, s, a);
 }
 
+// micro-benchmark kernel (the paper's axpy of Fig. 4): y = a x + y, float4
+// vectorised, grid sized to the SM count (persistent grid-stride loop)
+__global__ void __launch_bounds__(256) axpy_kernel(float a, const float4* __restrict__ x, float4* __restrict__ y,
+                                                   long long n4) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const float4 xv = x[i];
+    float4 yv = y[i];
+    yv.x = fmaf(a, xv.x, yv.x);
+    yv.y = fmaf(a, xv.y, yv.y);
+    yv.z = fmaf(a, xv.z, yv.z);
+    yv.w = fmaf(a, xv.w, yv.w);
+    y[i] = yv;
+  }
+}
+cudaError_t launch_axpy(float a, const float* x, float* y, long long n, cudaStream_t s) {
+  if (n % 4) return cudaErrorInvalidValue;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  axpy_kernel<<<nsm * 8, 256, 0, s>>>(a, reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y), n / 4);
+  return cudaGetLastError();
+}
+
 // local coil sums before the cross-rank all-reduce (world > 1)
 __global__ void coil_sum_kernel(const float2* __restrict__ S_all, int J, float2* S, int Q) {
   pdl_wait();

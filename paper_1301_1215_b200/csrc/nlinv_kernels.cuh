@@ -192,6 +192,7 @@ struct XchgArgs {
   int Q;
 };
 cudaError_t launch_xchg(const XchgArgs& a, cudaStream_t s);
+cudaError_t launch_axpy(float a, const float* x, float* y, long long n, cudaStream_t s);
 cudaError_t launch_rss_sum(int ng, const float* rss_all, int J, float* rss, cudaStream_t s);
 
 }  // namespace nlv

@@ -66,6 +66,7 @@ _SIGS = {
     "nlinv_plan_stats": (c_int, [c_void_p, ctypes.POINTER(Stats)]),
     "nlinv_debug_fft2d": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]),
     "nlinv_debug_k234_clusters": (c_int, [c_int]),
+    "nlinv_debug_axpy": (c_int, [c_float, c_void_p, c_void_p, c_ll, c_void_p]),
     "nlinv_plan_exchange_handle": (c_int, [c_void_p, ctypes.c_char_p]),
     "nlinv_plan_connect": (c_int, [c_void_p, ctypes.c_char_p]),
     "nlinv_plan_connect_local": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
@@ -121,6 +122,13 @@ def coil_partition(ncoils: int, world: int, rank: int):
     f, c = c_int(), c_int()
     _check(_lib.nlinv_coil_partition(ncoils, world, rank, ctypes.byref(f), ctypes.byref(c)))
     return f.value, c.value
+
+
+def axpy(a: float, x, y, stream=None):
+    """y = a x + y on float32 CUDA tensors (micro-benchmark entry nlinv_debug_axpy)."""
+    _check(_lib.nlinv_debug_axpy(float(a), c_void_p(x.data_ptr()), c_void_p(y.data_ptr()), int(x.numel()),
+                                 _stream_ptr(stream)))
+    return y
 
 
 def get_unique_id() -> bytes:

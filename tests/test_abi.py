@@ -87,6 +87,7 @@ def test_plan_create_validates_before_device():
     assert B._lib.nlinv_plan_exchange_handle(None, buf) == 1
     assert B._lib.nlinv_plan_connect(None, buf) == 1
     assert B._lib.nlinv_plan_connect_local(None, None) == 1
+    assert B._lib.nlinv_debug_axpy(1.0, None, None, 4, None) == 1
 
 
 def test_nccl_unique_id():

@@ -390,3 +390,14 @@ def test_table1_fft_counts_of_the_cuda_passes():
         chan_sums = prof.get("row_k4", {"launches": 0})["launches"]
         assert chan_sums == gold[name]["chan_sum"], (name, prof)
     plan.close()
+
+
+def test_axpy_micro_benchmark_kernel():
+    """SURVEY f4 (the paper's axpy): y = a x + y through nlinv_debug_axpy, exact in fp32 for
+    these operands (a x is a power-of-two scaling)."""
+    from paper_1301_1215_b200.nlinv import axpy
+    x = torch.from_numpy(synth.splitmix64_uniform(5, 1 << 20).astype(np.float32)).cuda()
+    y = torch.from_numpy(synth.splitmix64_uniform(6, 1 << 20).astype(np.float32)).cuda()
+    want = 0.5 * x.cpu().numpy() + y.cpu().numpy()
+    axpy(0.5, x, y)
+    assert np.array_equal(y.cpu().numpy(), want.astype(np.float32))

@@ -3,6 +3,9 @@
   * batched 2D FFT strong scaling: a fixed batch of ng^2 images split over the ranks, each rank
     transforming its share with libnlinv's centred 2D FFT (nlinv_debug_fft2d); time = max over
     ranks of CUDA-event time; reported as images/s and GB/s (one read + one write per image)
+  * axpy strong scaling (the paper's Fig. 4): y = a x + y over a fixed vector of 2^28
+    floats split over the ranks (libnlinv's float4 kernel, nlinv_debug_axpy); time = max over ranks;
+    GB/s counts 12 bytes per element (x, y read; y written)
   * collective transfer curves: torch.distributed (NCCL) all-reduce and broadcast of 8 B .. 64 MB
     float buffers, median of 20 after 5 warm-ups, bus bandwidth per NCCL's convention
 
@@ -20,6 +23,7 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 from paper_1301_1215_b200 import Plan, radial_mask  # noqa: E402
+from paper_1301_1215_b200.nlinv import axpy  # noqa: E402
 
 
 def ev_time(fn, reps=20, warm=5):
@@ -53,7 +57,15 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    out = {"world": world, "fft": [], "allreduce": [], "broadcast": []}
+    out = {"world": world, "fft": [], "axpy": [], "allreduce": [], "broadcast": []}
+    for n_total in (1 << 24, 1 << 28):
+        share = ((n_total + world - 1) // world + 3) // 4 * 4
+        xv = torch.ones(share, dtype=torch.float32, device="cuda")
+        yv = torch.zeros(share, dtype=torch.float32, device="cuda")
+        ms = maxr(ev_time(lambda: axpy(0.5, xv, yv)), world)
+        out["axpy"].append({"n": n_total, "per_rank": share, "ms": round(ms, 4),
+                            "GBps_total": round(12.0 * n_total / (ms * 1e-3) / 1e9, 1)})
+        del xv, yv
     for ng, batch in ((384, 96), (1024, 32)):
         share = (batch + world - 1) // world
         plan = Plan(ng, 1, radial_mask(ng, 4, 1, 0))
