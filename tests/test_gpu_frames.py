@@ -78,20 +78,22 @@ def band_errors(xg, xo, nbands=4):
 
 
 @pytest.mark.slow
-def test_c2_warm_stream_in_bench_configuration():
+@pytest.mark.parametrize("J,frames", [(12, 5), (32, 3)])
+def test_c2_warm_stream_in_bench_configuration(J, frames):
     """BASELINE config 2 exactly as bench.py runs it: 12 coils, 384^2, 15 spokes rotated over 5 turns
     (P_k changes every frame), moving phantom, 7 Newton x 10 CG, each frame warm-started from the
     previous frame's x as x_0 = x_ref, the CUDA graph replayed on torch's default stream.
-    The oracle runs its own fp64 chain from the same cold start. Five frames."""
+    The oracle runs its own fp64 chain from the same cold start. Five frames. J = 32: the first three
+    frames of the BASELINE config 4 stream (32 coils, the multi-task fused K5 pass)."""
     B = _B()
-    ng, J, S, T, K, L = 384, 12, 15, 5, 7, 10
+    ng, S, T, K, L = 384, 15, 5, 7, 10
     plan = B.Plan(ng, J, O.radial_mask(ng, S, T, 0))
     x = torch.empty(plan.x_shape, dtype=torch.complex64, device="cuda")
     img = torch.empty(plan.image_shape, dtype=torch.complex64, device="cuda")
     frame = torch.empty(plan.y_shape, dtype=torch.complex64, device="cuda")
     xo = O.initial_x(J, ng)
     worst = {}
-    for f in range(5):
+    for f in range(frames):
         _, _, y = synth.frame_inputs(J, ng, t=f)
         y = c64(y)
         mask = O.radial_mask(ng, S, T, f)
