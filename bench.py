@@ -274,15 +274,17 @@ def _run_ours(args):
     tname, tv = top
     tb = algo_bytes(tname, NG, plan.count) * tv["launches"]
     achieved = tb / (tv["ms"] / 1e3) / 1e9
-    traffic = ncu_ms = None
+    traffic = ncu_ms = ncu_ms_warm = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             tr = json.load(fh)
         traffic = tr.get(tname, {}).get("dram_bytes_per_launch")
         us = tr.get(tname, {}).get("avg_us_ncu")
         ncu_ms = us / 1e3 if us else None
+        usw = tr.get(tname, {}).get("avg_us_ncu_warm")
+        ncu_ms_warm = usw / 1e3 if usw else None
     except Exception:
-        traffic = ncu_ms = None
+        traffic = ncu_ms = ncu_ms_warm = None
     frame_bytes = sum(algo_bytes(k, NG, plan.count) * v["launches"] for k, v in prof.items())
     kernels = {k: {"launches": v["launches"], "ms": round(v["ms"], 4),
                    "share": round(v["ms"] / frame_ms, 4),
@@ -319,6 +321,12 @@ def _run_ours(args):
                          "avg_launch_ms": tv["ms"] / tv["launches"],
                          "ncu_avg_launch_ms": ncu_ms,
                          "frac_ncu": (round(tb / tv["launches"] / (ncu_ms / 1e3) / 1e9 / peak, 4) if ncu_ms else None),
+                         "ncu_avg_launch_ms_warm": ncu_ms_warm,
+                         "frac_ncu_warm": (round(tb / tv["launches"] / (ncu_ms_warm / 1e3) / 1e9 / peak, 4)
+                                           if ncu_ms_warm else None),
+                         "ncu_note": ("profiles/ncu_traffic.json: ncu launch list of one eager C2 frame, serialised; "
+                                      "cold = L2 flushed before every kernel, warm = --cache-control none (the L2 "
+                                      "state a frame really sees)"),
                          "share_of_frame": round(tv["ms"] / frame_ms, 4),
                          "frame_algorithmic_GBps": round(frame_bytes / (frame_ms / 1e3) / 1e9, 1),
                          "method": "one extra frame with every kernel bracketed by CUDA events (no graph)",

@@ -84,6 +84,7 @@ open(os.path.join(ROOT, "profiles", f"{tag}_launches.md"), "w").write("\n".join(
 traffic = {nm: {"dram_bytes_per_launch": (a["dram__bytes_read.sum"] + a["dram__bytes_write.sum"]) / a["n"],
                 "dram_bytes_per_launch_warm": (warm[nm]["dram__bytes_read.sum"] + warm[nm]["dram__bytes_write.sum"]) / warm[nm]["n"] if nm in warm else None,
                 "avg_us_ncu": a["gpu__time_duration.sum"] / a["n"] / 1e3,
+                "avg_us_ncu_warm": (warm[nm]["gpu__time_duration.sum"] / warm[nm]["n"] / 1e3) if nm in warm else None,
                 "source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum (cold = L2 flushed per kernel; warm = --cache-control none), tools/profile.sh, {tag}"}
            for nm, a in cold.items()}
 json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
