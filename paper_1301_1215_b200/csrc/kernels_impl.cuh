@@ -29,7 +29,13 @@ struct ColGeo {
   static constexpr int CW = (L % c0 == 0) ? c0 : ((L % 16 == 0 && c0 >= 16) ? 16 : 8);
   static constexpr int THREADS = CW * T;
   static constexpr size_t SMEM = sizeof(float2) * (size_t)L * (CW + 1) + 64 * sizeof(double);
-  static constexpr size_t SMEM_PF = SMEM + 64 * sizeof(double) + sizeof(float2) * (size_t)L * CW;   // k5cg_kernel
+  // k5cg_kernel: + the r / dx tile (pf) + the CTA's w^-1 columns folded by |k - L/2| (w^-1 is even in k - L/2):
+  // (L/2 + 1) x CW floats loaded once before griddepcontrol.wait instead of 2 x L x CW global reads per
+  // launch; used where it does not lower the CTAs per SM (2 at <= 115712 B per CTA)
+  static constexpr size_t PF0 = SMEM + 64 * sizeof(double) + sizeof(float2) * (size_t)L * CW;
+  static constexpr size_t WTAB = sizeof(float) * (size_t)(L / 2 + 1) * CW;
+  static constexpr bool kWTab = (PF0 + WTAB <= 115712) || (PF0 > 115712 && PF0 + WTAB <= 232448);
+  static constexpr size_t SMEM_PF = PF0 + (kWTab ? WTAB : 0);
 };
 
 
@@ -727,7 +733,8 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColAr
 // accumulates its absolute error and ruins late iterations (measured in an fp32 model: 5e-2 on
 // the C1 image vs 6e-5 with the direct <r_i,r_i>).
 template <int L, bool XP>
-__device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, float2* xb, float2* pf, double* red) {
+__device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, float2* xb, float2* pf, double* red,
+                                          const float* wt) {
   using C = Cfg<L>;
   using S = Sched<L>;
   constexpr int E = C::E, CW = ColGeo<L>::CW;
@@ -741,6 +748,23 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   const bool last = a.last_iter != 0, hasdx = a.iter > 0;
   const unsigned nb = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
   ColBuf<CW> buf{xb, c};
+  // w^-1 at k-space row k of this thread's column (global index i): the folded shared table or global memory
+  // Register e holds k = t + out_off(e); when T divides L/2 and every offset, k - L/2 has the sign of
+  // out_off(e) - L/2 for all t, so the table row is +-t + a compile-time constant (two base pointers)
+  constexpr bool kFold = ((L / 2) % C::T == 0) && ((L / S::RL) % C::T == 0);
+  const float* wpos = wt + t * CW + c;
+  const float* wneg = wt - t * CW + c;
+  auto w_at = [&](int e, int k, size_t i) -> float {
+    if constexpr (ColGeo<L>::kWTab && kFold) {
+      const int o = S::out_off(e);
+      return (o >= L / 2) ? wpos[(o - L / 2) * CW] : wneg[(L / 2 - o) * CW];
+    } else if constexpr (ColGeo<L>::kWTab) {
+      const int r = k >= L / 2 ? k - L / 2 : L / 2 - k;
+      return wt[r * CW + c];
+    } else {
+      return a.winv[i];
+    }
+  };
 
   // r (dx in the last iteration) was written by the previous CG iteration's pass, which completed
   // before the passes in between could run: the L2-only (cp.async.cg) prefetch is issued before
@@ -858,7 +882,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
 #pragma unroll
       for (int u = 0; u < CH; ++u) {
         const size_t i = (size_t)S::out_idx(t, e0 + u) * L + x;
-        wv[u] = a.winv[i];
+        wv[u] = w_at(e0 + u, S::out_idx(t, e0 + u), i);
         pv[u] = a.p[j * N + i];
       }
 #pragma unroll
@@ -1046,7 +1070,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
 #pragma unroll
       for (int u = 0; u < CH; ++u) {
         const size_t ii = (size_t)S::out_idx(t, e0 + u) * L + x;
-        wv[u] = a.winv[ii];
+        wv[u] = w_at(e0 + u, S::out_idx(t, e0 + u), ii);
         dv[u] = hasdx ? a.dx[j * N + ii] : make_float2(0.f, 0.f);
       }
 #pragma unroll
@@ -1125,9 +1149,22 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) k5cg_kernel(ColA
   float2* xb = tw + L;
   double* red = reinterpret_cast<double*>(xb + (size_t)L * CW);   // 128 doubles
   float2* pf = reinterpret_cast<float2*>(red + 128);
+  float* wt = reinterpret_cast<float*>(pf + (size_t)L * CW);
   trace_stamp(a.trace, 0);
+  if constexpr (ColGeo<L>::kWTab) {
+    // w^-1 is fixed for the plan: its folded columns join the twiddles' cp.async group, before the wait.
+    // Row r of the table = |k - L/2| = r, read from global row L/2 + r (row 0 for r = L/2)
+    constexpr int C4 = CW / 4;   // 16-byte chunks per row
+    const int x0 = blockIdx.x * CW;
+    for (int i = threadIdx.x; i < (L / 2 + 1) * C4; i += blockDim.x) {
+      const int r = i / C4, c4 = i - r * C4;
+      const int gy = (r == L / 2) ? 0 : L / 2 + r;
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(wt + r * CW + 4 * c4);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(a.winv + (size_t)gy * L + x0 + 4 * c4));
+    }
+  }
   tw_copy_async(tw, twg, L);
-  k5cg_task<L, XP>(a, tw, xb, pf, red);   // griddepcontrol.wait inside, after the r prefetch
+  k5cg_task<L, XP>(a, tw, xb, pf, red, wt);   // griddepcontrol.wait inside, after the r prefetch
 }
 
 // ------------------------------------------------------------------ row task (one (coil, Omega row) per group)
