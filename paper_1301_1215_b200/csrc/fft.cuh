@@ -375,8 +375,13 @@ __device__ __forceinline__ void pass_exchange(float2* v, int t, BUF& buf, SYNC s
 // Full length-L transform: registers in pass-0 input pattern -> registers in last-pass
 // output pattern. Unnormalised, X_k = sum_n x_n e^{DIR 2 pi i n k / L}.
 // ZM0: bit r set if every register slot m*R0 + r of the pass-0 input is structurally zero
-template <int L, int DIR, unsigned ZM0 = 0, class BUF, class SYNC>
-__device__ __forceinline__ void fft(float2* v, int t, const float2* tw, BUF& buf, SYNC sync) {
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+// hook() runs once every thread is past the last shared-memory exchange (the buffer is free again,
+// e.g. for an asynchronous bulk copy into it) while the last pass computes in registers
+template <int L, int DIR, unsigned ZM0 = 0, class BUF, class SYNC, class HOOK = NoHook>
+__device__ __forceinline__ void fft(float2* v, int t, const float2* tw, BUF& buf, SYNC sync, HOOK hook = HOOK{}) {
   using C = Cfg<L>;
   if constexpr (ZM0 == 0) {
     pass_compute<L, C::R0, 1, DIR>(v, t, tw);
@@ -385,13 +390,16 @@ __device__ __forceinline__ void fft(float2* v, int t, const float2* tw, BUF& buf
     for (int m = 0; m < C::E / C::R0; ++m) DFTZ<C::R0, DIR, ZM0>::run(&v[m * C::R0]);
   }
   pass_exchange<L, C::R0, 1, C::R1>(v, t, buf, sync);
+  if constexpr (C::NP == 2) hook();
   pass_compute<L, C::R1, C::R0, DIR>(v, t, tw);
   if constexpr (C::NP >= 3) {
     pass_exchange<L, C::R1, C::R0, C::R2>(v, t, buf, sync);
+    if constexpr (C::NP == 3) hook();
     pass_compute<L, C::R2, C::R0 * C::R1, DIR>(v, t, tw);
   }
   if constexpr (C::NP >= 4) {
     pass_exchange<L, C::R2, C::R0 * C::R1, C::R3>(v, t, buf, sync);
+    hook();
     pass_compute<L, C::R3, C::R0 * C::R1 * C::R2, DIR>(v, t, tw);
   }
 }

@@ -339,6 +339,26 @@ __device__ __forceinline__ void tma_tile_issue(uint64_t* mbar, float2* dst, cons
         ::"r"(d), "l"(tmap), "r"(x0), "r"(y0), "r"(j), "r"(mb) : "memory");
   }
 }
+// the same into an mbarrier already initialised (tma_bar_init) and made visible to the CTA
+__device__ __forceinline__ void tma_bar_init(uint64_t* mbar) {
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb) : "memory");
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_tile_issue_ready(uint64_t* mbar, float2* dst, const void* tmap, int x0, int j, int L,
+                                                     int CW) {
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic accesses of dst before the async copy
+  const uint32_t bytes = (uint32_t)(L * CW * 8);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bytes) : "memory");
+  const int box = L <= 256 ? L : (L % 256 == 0 ? 256 : 192);
+  for (int y0 = 0; y0 < L; y0 += box) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + (size_t)y0 * CW);
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+        ::"r"(d), "l"(tmap), "r"(x0), "r"(y0), "r"(j), "r"(mb) : "memory");
+  }
+}
 __device__ __forceinline__ void tma_tile_wait(uint64_t* mbar) {
   const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar);
   uint32_t done = 0;
@@ -771,6 +791,10 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   // griddepcontrol.wait and overlaps the drain of the previous pass
   bool pf_on = false, pf_tma = false;
   __shared__ alignas(8) uint64_t pf_bar;
+  // p tile by TMA into the exchange buffer once the column FFT no longer needs it (p is parked there)
+  __shared__ alignas(8) uint64_t pp_bar;
+  const bool p_tma = a.tmap_p != nullptr;
+  if (p_tma && tid == 0) tma_bar_init(&pp_bar);   // visible to the CTA at the FFT's first block barrier
   const void* tmap = last ? a.tmap_dx : a.tmap_r;
   if (tmap != nullptr && (!last || hasdx)) {   // TMA (UTMALDG): one thread issues the tile loads
     if (tid == 0) tma_tile_issue(&pf_bar, pf, tmap, tile * CW, j, L, CW);
@@ -867,10 +891,13 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   if (pf_on) tw_wait_keep1();
   else tw_wait();
   trace_stamp(a.trace, 1);
-  fft<L, -1, omega_in_zmask<L>()>(v, t, tw, buf, SyncBlock{});   // T4: Omega rows only
+  fft<L, -1, omega_in_zmask<L>()>(v, t, tw, buf, SyncBlock{}, [&] {   // T4: Omega rows only
+    if (p_tma && tid == 0) tma_tile_issue_ready(&pp_bar, xb, a.tmap_p, tile * CW, j, L, CW);
+  });
   trace_stamp(a.trace, 2);
   if (pf_on) prefetch_wait();   // the r / dx tile is complete (all threads' copies)
   if (pf_tma) tma_tile_wait(&pf_bar);
+  if (p_tma) tma_tile_wait(&pp_bar);
 
   // epilogue: A p_chat = w^-1 (-1)^k . + alpha p; p parked in the (now free) exchange buffer
   {
@@ -883,7 +910,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
       for (int u = 0; u < CH; ++u) {
         const size_t i = (size_t)S::out_idx(t, e0 + u) * L + x;
         wv[u] = w_at(e0 + u, S::out_idx(t, e0 + u), i);
-        pv[u] = a.p[j * N + i];
+        pv[u] = p_tma ? buf(S::out_idx(t, e0 + u)) : a.p[j * N + i];
       }
 #pragma unroll
       for (int u = 0; u < CH; ++u) {
@@ -891,7 +918,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
         const float2 val = cscale(v[e0 + u], wv[u] * sgn_of(k));
         const float2 o = make_float2(fmaf(a.alpha, pv[u].x, val.x), fmaf(a.alpha, pv[u].y, val.y));
         v[e0 + u] = o;
-        buf(k) = pv[u];
+        if (!p_tma) buf(k) = pv[u];
         d[1] += (double)pv[u].x * o.x + (double)pv[u].y * o.y;
         // <r_i, r_i> directly from the stored r_i (R19); the last iteration takes the previous
         // pass's partials of the r_i it wrote (rr_next below) instead of reading r again

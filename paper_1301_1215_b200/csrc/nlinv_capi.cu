@@ -488,7 +488,7 @@ static void plan_free(nlinv_plan pl) {
 
 // TMA descriptors of the chat blocks [J][ng][ng] (8-byte elements) of r and dx: box = one fused-pass
 // column tile (CW columns) x up to 256 rows x one coil. false if the driver entry point is missing.
-static bool make_tile_maps(int ng, int J, float2* r_chat, float2* dx_chat, CUtensorMap out[2]) {
+static bool make_tile_maps(int ng, int J, float2* r_chat, float2* dx_chat, float2* p_chat, CUtensorMap out[3]) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (!enc) {
     cudaDriverEntryPointQueryResult q;
@@ -505,8 +505,8 @@ static bool make_tile_maps(int ng, int J, float2* r_chat, float2* dx_chat, CUten
   const cuuint64_t strides[2] = {(cuuint64_t)ng * 8, (cuuint64_t)ng * ng * 8};
   const cuuint32_t box[3] = {(cuuint32_t)cw, (cuuint32_t)(ng <= 256 ? ng : (ng % 256 == 0 ? 256 : 192)), 1};
   const cuuint32_t es[3] = {1, 1, 1};
-  float2* bases[2] = {r_chat, dx_chat};
-  for (int k = 0; k < 2; ++k) {
+  float2* bases[3] = {r_chat, dx_chat, p_chat};
+  for (int k = 0; k < 3; ++k) {
     if (enc(&out[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, bases[k], dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
@@ -633,8 +633,8 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
       // TMA tile prefetch of r / dx in the fused pass (NLINV_TMA=0: cp.async instead)
       const char* tm = std::getenv("NLINV_TMA");
       if (ok && !(tm && tm[0] == '0')) {
-        CUtensorMap h[2];
-        if (make_tile_maps(nx, pl->J, pl->r + N, pl->dx + N, h)) {
+        CUtensorMap h[3];
+        if (make_tile_maps(nx, pl->J, pl->r + N, pl->dx + N, pl->p + N, h)) {
           ok &= alloc((void**)&pl->tmaps, sizeof(h));
           ok &= ok && cudaMemcpy(pl->tmaps, h, sizeof(h), cudaMemcpyHostToDevice) == cudaSuccess;
         }
@@ -1088,6 +1088,7 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
         if (pl->tmaps) {
           c5.tmap_r = pl->tmaps;
           c5.tmap_dx = pl->tmaps + 1;
+          c5.tmap_p = pl->tmaps + 2;
         }
         TRY(q.col(CK_K5CG, c5));
       }

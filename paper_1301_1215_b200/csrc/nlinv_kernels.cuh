@@ -116,6 +116,8 @@ struct ColArgs {
   const XPeers* xp;        // peer-memory exchange (world > 1 without NCCL): device copy; nullptr: off
   const void* tmap_r;      // k5cg: CUtensorMap (device, 64-B aligned) of the chat blocks of r / dx for the TMA
   const void* tmap_dx;     // tile prefetch; nullptr: cp.async prefetch
+  const void* tmap_p;      // k5cg: CUtensorMap of the chat blocks of p: the p tile lands in the FFT exchange buffer
+                           // (where p is parked) right after the column FFT's last exchange; nullptr: global loads
 };
 
 struct RowArgs {
