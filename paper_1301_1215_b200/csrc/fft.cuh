@@ -22,21 +22,83 @@
 namespace nlv {
 
 // ------------------------------------------------------------------ complex helpers
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// sm_100a has packed two-lane fp32 instructions (FADD2 / FMUL2 / FFMA2: one instruction, both halves of a
+// register pair, each lane IEEE round-to-nearest like FADD / FMUL / FFMA): a complex add is one
+// instruction instead of two. ptxas folds lane broadcasts and the re/im swap into operand modifiers
+// (.F32 / .LO_HI), so a complex multiply is two or three. Measured lane throughput equals the scalar
+// pipe's (tools/probe_f32x2), so the gain is issue slots, which bound these FFT passes.
+#ifndef NLV_SCALAR_FP
+__device__ __forceinline__ unsigned long long pk2(float x, float y) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ float2 up2(unsigned long long r) {
+  float2 a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return up2(r);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return up2(r);
+}
+
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return up2(r);
+}
+
+// lane-wise a * b + c, one rounding per lane
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)), "l"(pk2(c.x, c.y)));
+  return up2(r);
+}
+#else   // scalar reference of the same lane-wise operations (A/B builds)
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return make_float2(a.x * b.x, a.y * b.y); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  return make_float2(fmaf(a.x, b.x, c.x), fmaf(a.y, b.y, c.y));
+}
+#endif
+__device__ __forceinline__ float2 swap2(float2 a) { return make_float2(a.y, a.x); }
+__device__ __forceinline__ float2 bcast2(float s) { return make_float2(s, s); }
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return add2(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return sub2(a, b); }
+// a * b = b.x a + b.y (-a.y, a.x)
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+  return fma2(swap2(a), make_float2(-b.y, b.y), mul2(a, bcast2(b.x)));
 }
-// conj(a) * b
+// conj(a) * b = a.x b + a.y (b.y, -b.x)
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.x, b.y, -a.y * b.x));
+  return fma2(swap2(b), make_float2(a.y, -a.y), mul2(b, bcast2(a.x)));
 }
+// scalar on purpose: the packed form (FMUL2 with a broadcast scalar) gave wrong results in the
+// ng = 16 / 48 adjoint passes (measured, tools/dbg_adj.py); the scalar pair costs one extra FMUL
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 __device__ __forceinline__ float2 cneg_if(float2 a, bool neg) { return neg ? make_float2(-a.x, -a.y) : a; }
 // a * (DIR * i)
 template <int DIR>
 __device__ __forceinline__ float2 mul_dir_i(float2 a) {
   return DIR < 0 ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
+}
+// a + DIR i b and a - DIR i b, each one FFMA2 (b swapped, lane signs as an immediate pair)
+template <int DIR>
+__device__ __forceinline__ float2 cadd_i(float2 a, float2 b) {
+  return fma2(swap2(b), DIR < 0 ? make_float2(1.f, -1.f) : make_float2(-1.f, 1.f), a);
+}
+template <int DIR>
+__device__ __forceinline__ float2 csub_i(float2 a, float2 b) {
+  return fma2(swap2(b), DIR < 0 ? make_float2(-1.f, 1.f) : make_float2(1.f, -1.f), a);
 }
 // e^{DIR 2 pi i m / R} for compile-time-foldable m, R with 48 % R == 0 (R in {2,3,4,6,8,12,16})
 template <int DIR>
@@ -79,11 +141,10 @@ struct DFT<3, DIR> {
     const float s = DIR * 0.866025403784438647f;
     float2 t1 = cadd(a[1], a[2]);
     float2 t2 = csub(a[1], a[2]);
-    float2 m = make_float2(fmaf(-0.5f, t1.x, a[0].x), fmaf(-0.5f, t1.y, a[0].y));
-    float2 is = make_float2(-s * t2.y, s * t2.x);
+    float2 m = fma2(bcast2(-0.5f), t1, a[0]);
     a[0] = cadd(a[0], t1);
-    a[1] = cadd(m, is);
-    a[2] = csub(m, is);
+    a[1] = fma2(swap2(t2), make_float2(-s, s), m);   // m + i s t2
+    a[2] = fma2(swap2(t2), make_float2(s, -s), m);   // m - i s t2
   }
 };
 
@@ -93,11 +154,11 @@ struct DFT<4, DIR> {
     float2 t0 = cadd(a[0], a[2]);
     float2 t1 = csub(a[0], a[2]);
     float2 t2 = cadd(a[1], a[3]);
-    float2 t3 = mul_dir_i<DIR>(csub(a[1], a[3]));
+    float2 d3 = csub(a[1], a[3]);
     a[0] = cadd(t0, t2);
     a[2] = csub(t0, t2);
-    a[1] = cadd(t1, t3);
-    a[3] = csub(t1, t3);
+    a[1] = cadd_i<DIR>(t1, d3);
+    a[3] = csub_i<DIR>(t1, d3);
   }
 };
 
@@ -112,10 +173,13 @@ __device__ __forceinline__ float2 mul_root48(float2 a, int k48) {
   if (k == 12) return mul_dir_i<DIR>(a);                       // e^{DIR i pi/2} = DIR i
   if (k == 36) return mul_dir_i<-DIR>(a);
   constexpr float h = 0.707106781186547524f;
-  if (k == 6) return DIR < 0 ? make_float2((a.x + a.y) * h, (a.y - a.x) * h) : make_float2((a.x - a.y) * h, (a.x + a.y) * h);
-  if (k == 18) return DIR < 0 ? make_float2((a.y - a.x) * h, -(a.x + a.y) * h) : make_float2(-(a.x + a.y) * h, (a.x - a.y) * h);
-  if (k == 30) return DIR < 0 ? make_float2(-(a.x + a.y) * h, (a.x - a.y) * h) : make_float2((a.y - a.x) * h, -(a.x + a.y) * h);
-  if (k == 42) return DIR < 0 ? make_float2((a.x - a.y) * h, (a.x + a.y) * h) : make_float2((a.x + a.y) * h, (a.y - a.x) * h);
+  // eighth turns: h (a + swap(a) (s0, s1)) with the lane signs of each case (one FFMA2 + one FMUL2)
+  if (k == 6) return DIR < 0 ? cscale(fma2(swap2(a), make_float2(1.f, -1.f), a), h) : cscale(fma2(swap2(a), make_float2(-1.f, 1.f), a), h);
+  if (k == 18) return DIR < 0 ? cscale(fma2(swap2(a), make_float2(1.f, -1.f), make_float2(-a.x, -a.y)), h)
+                              : cscale(fma2(swap2(a), make_float2(-1.f, 1.f), make_float2(-a.x, -a.y)), h);
+  if (k == 30) return DIR < 0 ? cscale(fma2(swap2(a), make_float2(-1.f, 1.f), make_float2(-a.x, -a.y)), h)
+                              : cscale(fma2(swap2(a), make_float2(1.f, -1.f), make_float2(-a.x, -a.y)), h);
+  if (k == 42) return DIR < 0 ? cscale(fma2(swap2(a), make_float2(-1.f, 1.f), a), h) : cscale(fma2(swap2(a), make_float2(1.f, -1.f), a), h);
   return cmul(a, unit_root48<DIR>(k));
 }
 
@@ -207,11 +271,20 @@ struct DFTZ<4, DIR, ZM> {
     const float2 t0 = zadd<z0, z2>(a[0], a[2]);
     const float2 t1 = zsub<z0, z2>(a[0], a[2]);
     const float2 t2 = zadd<z1, z3>(a[1], a[3]);
-    const float2 t3 = mul_dir_i<DIR>(zsub<z1, z3>(a[1], a[3]));
+    const float2 d3 = zsub<z1, z3>(a[1], a[3]);
     a[0] = zadd<zt0, zt2>(t0, t2);
     a[2] = zsub<zt0, zt2>(t0, t2);
-    a[1] = zadd<zt0, zt2>(t1, t3);
-    a[3] = zsub<zt0, zt2>(t1, t3);
+    if constexpr (zt0 && zt2) {
+      a[1] = a[3] = make_float2(0.f, 0.f);
+    } else if constexpr (zt2) {
+      a[1] = a[3] = t1;
+    } else if constexpr (zt0) {
+      a[1] = mul_dir_i<DIR>(d3);
+      a[3] = mul_dir_i<-DIR>(d3);
+    } else {
+      a[1] = cadd_i<DIR>(t1, d3);
+      a[3] = csub_i<DIR>(t1, d3);
+    }
   }
 };
 // group mask of the n2-th stride-R2 subsequence (n = R2 n1 + n2) of a length-R1*R2 input
