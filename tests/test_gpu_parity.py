@@ -323,6 +323,7 @@ def test_reconstruct_c2_full_frame():
 VARIANTS = {
     "fused (default, one grid barrier per CG iteration)": {},
     "fused, cluster-fused K2-K3-K4 (DSMEM transposes)": {"NLINV_K234": "1"},
+    "fused, cp.async tile prefetch instead of TMA (NLINV_TMA=0)": {"NLINV_TMA": "0"},
     "unfused K1/K5, textbook two reductions": {"NLINV_FUSE_K5": "0"},
     "unfused K1/K5, single reduction": {"NLINV_FUSE_K5": "0", "NLINV_CG1": "1"},
     "multi-GPU code path (single reduction), one-rank NCCL communicator": {"NLINV_FORCE_NCCL": "1"},
