@@ -765,6 +765,9 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   const int tid = threadIdx.x, c = tid % CW, t = tid / CW;
   const int tile = blockIdx.x, j = blockIdx.y;
   const int x = tile * CW + c;
+  // CTA rows j >= J carry no coil tile, only their stripe of the rho block: with few local coils (a
+  // coil-sharded rank) the N-element rho stripe work would otherwise fall on 24 J CTAs (k5cg_rows)
+  const bool tcta = j < a.J;
   const bool last = a.last_iter != 0, hasdx = a.iter > 0;
   const unsigned nb = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
   ColBuf<CW> buf{xb, c};
@@ -793,10 +796,12 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   __shared__ alignas(8) uint64_t pf_bar;
   // p tile by TMA into the exchange buffer once the column FFT no longer needs it (p is parked there)
   __shared__ alignas(8) uint64_t pp_bar;
-  const bool p_tma = a.tmap_p != nullptr;
+  const bool p_tma = a.tmap_p != nullptr && tcta;
   if (p_tma && tid == 0) tma_bar_init(&pp_bar);   // visible to the CTA at the FFT's first block barrier
   const void* tmap = last ? a.tmap_dx : a.tmap_r;
-  if (tmap != nullptr && (!last || hasdx)) {   // TMA (UTMALDG): one thread issues the tile loads
+  if (!tcta) {
+    // rho-only CTA: no tile prefetch
+  } else if (tmap != nullptr && (!last || hasdx)) {   // TMA (UTMALDG): one thread issues the tile loads
     if (tid == 0) tma_tile_issue(&pf_bar, pf, tmap, tile * CW, j, L, CW);
     pf_tma = true;
   } else if (!last) {
@@ -821,7 +826,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   float2 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    if (in_is_omega<L>(e)) {
+    if (in_is_omega<L>(e) && tcta) {
       const int yr = S::in_idx(t, e);
       v[e] = cneg_if(a.in[j * H + (size_t)(yr - q) * L + x], yr & 1);
     } else {
@@ -833,8 +838,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   // Dot partials in fp64 per term: fp32 products underflow once CG has driven r, p to ~1e-20
   // (the first Newton step from rho = 1, chat = 0 reaches ||r|| ~ 1e-30), giving 0/0.
   double d[NV] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  constexpr int NTILE = L / CW;
-  const int nstripe = a.J * NTILE, stripe = j * NTILE + tile;
+  const int nstripe = (int)nb, stripe = (int)bid;   // one stripe per CTA (tile and rho-only CTAs)
   const size_t chunk = (N + nstripe - 1) / nstripe;
   const size_t lo = (size_t)stripe * chunk, hi = (lo + chunk < N) ? lo + chunk : N;
   // stripe values stay in registers when the stripe is <= SR elements per thread (C2: 2); the
@@ -891,16 +895,17 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   if (pf_on) tw_wait_keep1();
   else tw_wait();
   trace_stamp(a.trace, 1);
-  fft<L, -1, omega_in_zmask<L>()>(v, t, tw, buf, SyncBlock{}, [&] {   // T4: Omega rows only
-    if (p_tma && tid == 0) tma_tile_issue_ready(&pp_bar, xb, a.tmap_p, tile * CW, j, L, CW);
-  });
+  if (tcta)
+    fft<L, -1, omega_in_zmask<L>()>(v, t, tw, buf, SyncBlock{}, [&] {   // T4: Omega rows only
+      if (p_tma && tid == 0) tma_tile_issue_ready(&pp_bar, xb, a.tmap_p, tile * CW, j, L, CW);
+    });
   trace_stamp(a.trace, 2);
   if (pf_on) prefetch_wait();   // the r / dx tile is complete (all threads' copies)
   if (pf_tma) tma_tile_wait(&pf_bar);
   if (p_tma) tma_tile_wait(&pp_bar);
 
   // epilogue: A p_chat = w^-1 (-1)^k . + alpha p; p parked in the (now free) exchange buffer
-  {
+  if (tcta) {
     constexpr int CH = 8;
 #pragma unroll
     for (int e0 = 0; e0 < E; e0 += CH) {
@@ -1055,16 +1060,18 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
 
   if (last) {
     // Newton update x_{n+1} = x_n + dx + gamma_{L-1} p_{L-1} (Eq. 3) on this tile and stripe
+    if (tcta) {
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int k = S::out_idx(t, e);
-      const size_t i = j * N + (size_t)k * L + x;
-      const float2 pv = buf(k);
-      const float2 dv = hasdx ? pf[k * CW + c] : make_float2(0.f, 0.f);
-      float2 xv = a.xc[i];
-      xv.x += fmaf(gamma, pv.x, dv.x);
-      xv.y += fmaf(gamma, pv.y, dv.y);
-      a.xc[i] = xv;
+      for (int e = 0; e < E; ++e) {
+        const int k = S::out_idx(t, e);
+        const size_t i = j * N + (size_t)k * L + x;
+        const float2 pv = buf(k);
+        const float2 dv = hasdx ? pf[k * CW + c] : make_float2(0.f, 0.f);
+        float2 xv = a.xc[i];
+        xv.x += fmaf(gamma, pv.x, dv.x);
+        xv.y += fmaf(gamma, pv.y, dv.y);
+        a.xc[i] = xv;
+      }
     }
     auto newton_rho = [&](size_t i, float2 pv) {
       const float2 dv = hasdx ? a.rho_dx[i] : make_float2(0.f, 0.f);
@@ -1088,7 +1095,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   // r_{i+1} = r - gamma Ap; dx += gamma p; p_{i+1} = r_{i+1} + beta p (in place); t = w^-1 p_{i+1}
   // (K1 prologue). <r_{i+1}, r_{i+1}> partials of the stored r_{i+1} for the last iteration (rr_next)
   double rrn_r = 0.0, rrn_c = 0.0;
-  {
+  if (tcta) {
     constexpr int CH = 8;
 #pragma unroll
     for (int e0 = 0; e0 < E; e0 += CH) {
@@ -1157,6 +1164,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
     }
   }
   __syncthreads();   // every parked p has been read: xb becomes the exchange buffer again
+  if (!tcta) return;
   out_to_in<L>(v, t, buf, SyncBlock{});
   fft<L, +1>(v, t, tw, buf, SyncBlock{});
 #pragma unroll
@@ -1782,7 +1790,29 @@ static cudaError_t launch_k5cg_t(const ColArgs& a, const float2* tw, cudaStream_
   const size_t smem = ColGeo<L>::SMEM_PF;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_coop(kern, dim3(L / ColGeo<L>::CW, a.J), dim3(ColGeo<L>::THREADS), smem, s, true, a, tw);
+  return launch_coop(kern, dim3(L / ColGeo<L>::CW, a.k5_rows > a.J ? a.k5_rows : a.J), dim3(ColGeo<L>::THREADS), smem,
+                     s, true, a, tw);
+}
+// CTA rows of the fused pass: J coil rows; when the coil CTAs alone would leave more than 8 rho elements
+// per thread (few local coils: a coil-sharded rank), topped up with rho-only rows to 2 per thread (N / 512
+// CTAs), within one co-resident wave. Measured at 384^2 (frames/s, J = 1 / 2 / 4 / 12): 347 / 352 / 346 / 262
+// against 249 / 316 / 346 / 263 without rho-only rows; topping up J = 4 (6 per thread) measured slower.
+template <int L>
+static int k5cg_rows_l(int J) {
+  int dev = 0, nsm = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k5cg_kernel<L, false>, ColGeo<L>::THREADS,
+                                                    ColGeo<L>::SMEM_PF) != cudaSuccess)
+    return J;
+  constexpr int NT = L / ColGeo<L>::CW;
+  constexpr long long N = (long long)L * L, TH = ColGeo<L>::THREADS;
+  if (N <= 8 * TH * NT * (long long)J) return J;
+  const long long want = (N + 2 * TH - 1) / (2 * TH);
+  long long rows = (want + NT - 1) / NT;
+  const long long cap = (long long)per * nsm / NT;
+  if (rows > cap) rows = cap;
+  return rows > J ? (int)rows : J;
 }
 
 template <int L, int MODE>
@@ -2053,6 +2083,7 @@ static cudaError_t launch_fft2d_l(const float2* in, float2* out, int batch, int 
                                cudaStream_t s);                                                 \
   int col_tiles_##L();                                                                          \
   bool k5cg_fusable_##L(int J);                                                                  \
+  int k5cg_rows_##L(int J);                                                                      \
   bool k234_ok_##L();                                                                            \
   cudaError_t launch_k234_##L(const RowArgs& a, const float2* tw, cudaStream_t s);              \
   int k234_max_clusters_##L();                                                                   \
@@ -2070,6 +2101,7 @@ static cudaError_t launch_fft2d_l(const float2* in, float2* out, int batch, int 
   }                                                                                              \
   int col_tiles_##L() { return L / ColGeo<L>::CW; }                                             \
   bool k5cg_fusable_##L(int J) { return k5cg_fusable_l<L>(J); }                                  \
+  int k5cg_rows_##L(int J) { return k5cg_rows_l<L>(J); }                                          \
   bool k234_ok_##L() { return k234_ok_l<L>(); }                                                  \
   cudaError_t launch_k234_##L(const RowArgs& a, const float2* tw, cudaStream_t s) { return launch_k234_l<L>(a, tw, s); } \
   int k234_max_clusters_##L() { return k234_max_clusters_l<L>(); }                                 \

@@ -70,6 +70,7 @@ struct nlinv_plan_s {
   char* xwin = nullptr;                   // this rank's exchange window (IPC-exportable)
   std::vector<void*> ipc_open;            // peer windows opened through CUDA IPC
   bool fused = false;                     // fused K5 + CG + K1 pass, one grid barrier (k5cg_kernel, R19)
+  int k5_rows = 0;                        // its CTA rows (>= J; the extra rows carry rho stripes only)
   bool k234 = false;                      // cluster-fused K2 -> K3 -> K4 in the fused CG loop (k234_kernel)
   bool cg1 = false;                       // unfused CG: one (grouped) scalar all-reduce per iteration (R19)
   unsigned* kbar = nullptr;               // its grid barrier
@@ -628,6 +629,7 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
     const char* kc = std::getenv("NLINV_K234");
     pl->k234 = pl->fused && (kc && kc[0] == '1') && k234_supported(nx);
     if (pl->fused) {
+      pl->k5_rows = k5cg_rows(nx, pl->J);
       ok &= alloc((void**)&pl->kbar, sizeof(unsigned) * 4);
       ok &= alloc((void**)&pl->kpart, sizeof(double) * 10 * kMaxRedBlocks);   // 8 dots + 2 <r_{i+1},r_{i+1}>
       // TMA tile prefetch of r / dx in the fused pass (NLINV_TMA=0: cp.async instead)
@@ -1084,6 +1086,7 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
         c5.xc = x + N;
         c5.x_rho = x;
         c5.bar_count = pl->kbar;
+        c5.k5_rows = pl->k5_rows;
         c5.fpart = pl->kpart;
         if (pl->tmaps) {
           c5.tmap_r = pl->tmaps;

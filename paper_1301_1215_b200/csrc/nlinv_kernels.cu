@@ -369,6 +369,12 @@ bool k5cg_fusable(int ng, int J) {
 #undef X
   return false;
 }
+int k5cg_rows(int ng, int J) {
+#define X(L) if (ng == L) return k5cg_rows_##L(J);
+  NLV_FOR_EACH_NG(X)
+#undef X
+  return J;
+}
 bool k234_supported(int ng) {
 #define X(L) if (ng == L) return k234_ok_##L();
   NLV_FOR_EACH_NG(X)

@@ -116,6 +116,7 @@ struct ColArgs {
   const XPeers* xp;        // peer-memory exchange (world > 1 without NCCL): device copy; nullptr: off
   const void* tmap_r;      // k5cg: CUtensorMap (device, 64-B aligned) of the chat blocks of r / dx for the TMA
   const void* tmap_dx;     // tile prefetch; nullptr: cp.async prefetch
+  int k5_rows;              // k5cg: CTA rows (>= J; rows >= J are rho-only CTAs)
   const void* tmap_p;      // k5cg: CUtensorMap of the chat blocks of p: the p tile lands in the FFT exchange buffer
                            // (where p is parked) right after the column FFT's last exchange; nullptr: global loads
 };
@@ -175,6 +176,7 @@ cudaError_t launch_grid_radial(const float2* raw, int J, int nraw, const int* ce
 cudaError_t launch_scatter_samples(const float2* samples, const int* idx, const int* nnz, int nnz_cap, int J,
                                    size_t N, float2* y, cudaStream_t s);
 bool k5cg_fusable(int ng, int J);
+int k5cg_rows(int ng, int J);   // CTA rows of the fused pass (>= J: the extra rows carry rho stripes only)
 // cluster-fused K2 -> K3 -> K4 (one thread-block cluster per coil, DSMEM transposes)
 bool k234_supported(int ng);
 cudaError_t launch_k234(int ng, const RowArgs& a, const float2* tw, cudaStream_t s);

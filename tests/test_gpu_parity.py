@@ -305,6 +305,28 @@ def test_reconstruct_c4_newton_step_32_coils():
     plan.close()
 
 
+@pytest.mark.parametrize("J", [1, 2])
+def test_reconstruct_few_local_coils(J):
+    """A coil-sharded rank's load at the C2 grid (1 or 2 local coils, 384^2): the fused pass tops its CTA
+    grid up with rho-only CTAs (k5cg_rows) so the replicated rho block's stripes stay small; 2 Newton x 4 CG
+    (the last CG iteration's Newton update included), then a warm second frame, vs the oracle."""
+    B = _B()
+    ng = 384
+    y, mask = _frame(ng, J, 15, 5)
+    plan = B.Plan(ng, J, mask)
+    x, img = plan.reconstruct(dev(y), None, 2, 4)
+    xo, io, hist = _oracle_recon(y, mask, 2, 4)
+    assert rel(host(img), io) < 1e-4
+    assert rel(host(x), xo) < 1e-4
+    assert np.allclose(plan.stats()["residual"], hist, rtol=1e-4)
+    y1, m1 = _frame(ng, J, 15, 5, f=1)
+    plan.set_mask(torch.from_numpy(m1).cuda())
+    x1, img1 = plan.reconstruct(dev(y1), x, 1, 4)
+    xo1, io1, _ = _oracle_recon(y1, m1, 1, 4, prior=c64(host(x)))
+    assert rel(host(img1), io1) < 1e-4
+    plan.close()
+
+
 @pytest.mark.slow
 def test_reconstruct_c2_full_frame():
     """BASELINE config 2: the full 7 Newton x 10 CG frame vs the oracle (about a minute of CPU)."""
