@@ -7,7 +7,7 @@ import numpy as np, torch
 import synth
 from paper_1301_1215_b200 import Plan, radial_mask
 mode = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-NG, J = 384, 12
+NG, J = 384, int(os.environ.get("J", 12))
 plan = Plan(NG, J, radial_mask(NG, 15, 5, 0))
 _, _, y = synth.frame_inputs(J, NG)
 yd = torch.from_numpy(y.astype(np.complex64)).cuda()
