@@ -1071,6 +1071,8 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
         xv.x += fmaf(gamma, pv.x, dv.x);
         xv.y += fmaf(gamma, pv.y, dv.y);
         a.xc[i] = xv;
+        // the next set point's column pass (CK_IFFT_W) folded in: w^-1 x_{n+1} of this tile -> T1 below
+        v[e] = cscale(xv, w_at(e, k, (size_t)k * L + x) * sgn_of(k));
       }
     }
     auto newton_rho = [&](size_t i, float2 pv) {
@@ -1088,6 +1090,20 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
       }
     } else {
       for (size_t i = lo + tid; i < hi; i += blockDim.x) newton_rho(i, a.rho_a[i]);
+    }
+    if (!a.fold_sp) return;
+    // column IFFT of w^-1 x_{n+1} restricted to the Omega rows, into T1: what the next Newton step's set
+    // point (or the frame's RSS image) would compute in its own column pass
+    __syncthreads();   // every parked p has been read: xb becomes the exchange buffer again
+    if (!tcta) return;
+    out_to_in<L>(v, t, buf, SyncBlock{});
+    fft<L, +1>(v, t, tw, buf, SyncBlock{});
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (out_is_omega<L>(e)) {
+        const int k = S::out_idx(t, e);
+        a.t1[j * H + (size_t)(k - q) * L + x] = cscale(v[e], invL * sgn_of(k));
+      }
     }
     return;
   }

@@ -852,12 +852,13 @@ struct Enq {
 
 // c_j on Omega and rho|Omega of the point x. fwd_out != NULL: also the first
 // half of F(x) (row FFT of rho c_j) into fwd_out.
-nlinv_status enq_set_point(Enq& q, const float2* x, float2* fwd_out) {
+// t_ready: tA already holds the column pass of x (the previous fused Newton update folded it in).
+nlinv_status enq_set_point(Enq& q, const float2* x, float2* fwd_out, bool t_ready = false) {
   nlinv_plan pl = q.pl;
   ColArgs ca{};
   ca.src = x + pl->N;
   ca.out = pl->tA;
-  TRY(q.col(CK_IFFT_W, ca));
+  if (!t_ready) TRY(q.col(CK_IFFT_W, ca));
   RowArgs ra{};
   ra.in = pl->tA;
   ra.xrho = x;
@@ -996,10 +997,12 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
     TRY(q.kern("init_x", [&] { return launch_init_x(x, (long long)N, (long long)tot, q.s); }));
   }
   double alpha_d = pl->prm.alpha0;
+  bool sp_ready = false;   // tA holds the set-point column pass of x (folded into the fused Newton update)
   for (int nstep = 0; nstep < K; ++nstep, alpha_d *= pl->prm.q) {
     const float alpha = (float)alpha_d;
     // set point + forward head
-    TRY(enq_set_point(q, x, pl->tB));
+    TRY(enq_set_point(q, x, pl->tB, sp_ready));
+    sp_ready = false;
     // residual r = P(y - F x) and the adjoint head on it (Table 1 rows F and DF^H)
     ColArgs ca{};
     ca.in = pl->tB;
@@ -1087,6 +1090,7 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
         c5.x_rho = x;
         c5.bar_count = pl->kbar;
         c5.k5_rows = pl->k5_rows;
+        c5.fold_sp = (it == L - 1) ? 1 : 0;
         c5.fpart = pl->kpart;
         if (pl->tmaps) {
           c5.tmap_r = pl->tmaps;
@@ -1095,6 +1099,7 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
         }
         TRY(q.col(CK_K5CG, c5));
       }
+      sp_ready = L >= 1;
       continue;
     }
     // CG: L iterations of the normal operator + vector updates
@@ -1121,7 +1126,7 @@ nlinv_status enq_reconstruct(Enq& q, const float2* frame, const float2* prior, i
     ColArgs ca{};
     ca.src = x + N;
     ca.out = pl->tA;
-    TRY(q.col(CK_IFFT_W, ca));
+    if (!sp_ready) TRY(q.col(CK_IFFT_W, ca));
     RowArgs ra{};
     ra.in = pl->tA;
     ra.xrho = x;

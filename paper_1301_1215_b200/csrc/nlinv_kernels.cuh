@@ -117,6 +117,7 @@ struct ColArgs {
   const void* tmap_r;      // k5cg: CUtensorMap (device, 64-B aligned) of the chat blocks of r / dx for the TMA
   const void* tmap_dx;     // tile prefetch; nullptr: cp.async prefetch
   int k5_rows;              // k5cg: CTA rows (>= J; rows >= J are rho-only CTAs)
+  int fold_sp;              // k5cg, last CG iteration: also the set-point column pass of x_{n+1} into t1
   const void* tmap_p;      // k5cg: CUtensorMap of the chat blocks of p: the p tile lands in the FFT exchange buffer
                            // (where p is parked) right after the column FFT's last exchange; nullptr: global loads
 };
