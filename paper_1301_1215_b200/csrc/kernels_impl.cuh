@@ -1526,7 +1526,13 @@ __global__ void __launch_bounds__(256, NLV_MINB) row_kernel(RowArgs a, const flo
   } else if constexpr (MODE == RK_K2) {
     // per-group staging of c_j|Omega, rho|Omega, p_rho|Omega after the exchange buffers (RowGeo::SMEM_K2)
     const int gpc = blockDim.x / Cfg<L>::T;
-    row_task<L, MODE>(a, blockIdx.x * gpc, tw, xb, true, xb + (size_t)L * gpc);
+    if (a.stage) {
+      row_task<L, MODE>(a, blockIdx.x * gpc, tw, xb, true, xb + (size_t)L * gpc);
+    } else {
+      pdl_wait();
+      pdl_trigger();
+      row_task<L, MODE>(a, blockIdx.x * gpc, tw, xb, true);
+    }
   } else {
     pdl_wait();
     pdl_trigger();
@@ -1879,10 +1885,21 @@ static cudaError_t launch_row_t(const RowArgs& a0, const float2* tw, cudaStream_
     const int gpc = row_pairs_per_cta<L>();
     const int grid = (a0.J * (L / 2) + gpc - 1) / gpc;
     if constexpr (MODE == RK_K2) {
+      // staging the pre-wait operands costs shared memory: only where the grid is one wave anyway or two
+      // staged CTAs still fit an SM (above L2, e.g. 1024^2 x 32, it would cap the pass at one CTA per SM)
+      static int nsm = 0;
+      if (nsm == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      }
       const size_t sm2 = sizeof(float2) * ((size_t)L * (gpc + 1) + (size_t)gpc * 3 * (L / 2));
-      if (sm2 > smem && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) != cudaSuccess)
+      RowArgs a = a0;
+      a.stage = (sm2 <= 115712 || grid <= nsm) ? 1 : 0;
+      const size_t shm = a.stage ? (sm2 > smem ? sm2 : smem) : smem;
+      if (shm > smem && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm)) != cudaSuccess)
         return e;
-      return launch_k(kern, dim3(grid), dim3(gpc * Cfg<L>::T), sm2 > smem ? sm2 : smem, s, a0, tw);
+      return launch_k(kern, dim3(grid), dim3(gpc * Cfg<L>::T), shm, s, a, tw);
     }
     return launch_k(kern, dim3(grid), dim3(gpc * Cfg<L>::T), smem, s, a0, tw);
   }

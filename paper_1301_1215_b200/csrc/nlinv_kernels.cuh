@@ -135,6 +135,7 @@ struct RowArgs {
   int J;
   const XPeers* xp;        // peer-memory exchange: K4 writes its coil-sum plane into the window and publishes
   int kchunk;              // K4 coils per CTA (set by the launcher)
+  int stage;               // K2: stage c|Omega, rho|Omega, p_rho rows in shared memory (set by the launcher)
 };
 int k4_planes(int ng, int J);  // number of K4 coil-sum planes
 
