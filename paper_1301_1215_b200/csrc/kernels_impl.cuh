@@ -306,6 +306,20 @@ __device__ __forceinline__ void prefetch_wait() {
   __syncthreads();
 }
 
+// L2 prefetch of the column tile the CTA one resident wave later will transform (grids of several waves,
+// data above L2): the next wave finds its input in L2 while this wave computes. wave = CTAs per resident
+// wave (0: off); one prefetch per row segment (threads of column 0).
+template <int L>
+__device__ __forceinline__ void prefetch_next_wave_cols(const float2* base, size_t plane, int wave, int rlo, int rhi) {
+  constexpr int CW = ColGeo<L>::CW;
+  if (wave <= 0 || threadIdx.x % CW != 0) return;
+  const unsigned nb = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x, nxt = bid + (unsigned)wave;
+  if (nxt >= nb) return;
+  const float2* d = base + (size_t)(nxt / gridDim.x) * plane + (size_t)(nxt % gridDim.x) * CW;
+  for (int r = rlo + (int)(threadIdx.x / CW); r < rhi; r += (int)(blockDim.x / CW))
+    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(d + (size_t)r * L));
+}
+
 // Column-tile prefetch: rows 0..L-1, columns x0..x0+CW-1 of one [L][L] c64 image into shared
 // memory laid out [row][CW] (the ColBuf layout: thread (t, c) later reads its rows k at
 // dst[k * CW + c]); 16-byte cp.async.cg (L2 only), one commit group.
@@ -1790,6 +1804,20 @@ static cudaError_t launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, si
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
 }
 
+// CTAs per resident wave of a column kernel, when its grid (L/CW x batch) spans more than one wave and its
+// data exceed L2 (next-wave L2 prefetch); 0 otherwise
+template <int L, class K>
+static int col_wave(K kern, size_t smem, int batch) {
+  int dev = 0, nsm = 0, per = 0, l2 = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, ColGeo<L>::THREADS, smem) != cudaSuccess || per < 1) return 0;
+  const long long wave = (long long)per * nsm, grid = (long long)(L / ColGeo<L>::CW) * batch;
+  const double bytes = 8.0 * L * L * batch;
+  return (grid > wave && bytes > 0.5 * l2) ? (int)wave : 0;
+}
+
 // can the fused K5 + CG + K1 pass (k5cg_kernel) run as one co-resident (cooperative) wave?
 template <int L>
 static bool k5cg_fusable_l(int J) {
@@ -2053,7 +2081,8 @@ __global__ void __launch_bounds__(256) fft_rows_tw_kernel(const float2* __restri
 }
 
 template <int L, int DIR>
-__global__ void __launch_bounds__(ColGeo<L>::THREADS) fft_cols_tw_kernel(float2* data, const float2* __restrict__ twg) {
+__global__ void __launch_bounds__(ColGeo<L>::THREADS) fft_cols_tw_kernel(float2* data, const float2* __restrict__ twg,
+                                                                         int wave) {
   using C = Cfg<L>;
   using S = Sched<L>;
   constexpr int E = C::E, CW = ColGeo<L>::CW;
@@ -2066,6 +2095,7 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS) fft_cols_tw_kernel(float2*
   const int tid = threadIdx.x, c = tid % CW, t = tid / CW;
   const int x = blockIdx.x * CW + c;
   float2* d = data + (size_t)blockIdx.y * N;
+  prefetch_next_wave_cols<L>(data, N, wave, 0, L);
   ColBuf<CW> buf{xb, c};
   float2 v[E];
 #pragma unroll
@@ -2096,14 +2126,14 @@ static cudaError_t launch_fft2d_l(const float2* in, float2* out, int batch, int 
     if ((e = cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm)) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm)) != cudaSuccess) return e;
     rk<<<(nrows + gpc - 1) / gpc, gpc * T, rsm, s>>>(in, out, nrows, tw);
-    ck<<<dim3(L / ColGeo<L>::CW, batch), ColGeo<L>::THREADS, csm, s>>>(out, tw);
+    ck<<<dim3(L / ColGeo<L>::CW, batch), ColGeo<L>::THREADS, csm, s>>>(out, tw, col_wave<L>(ck, csm, batch));
   } else {
     auto rk = fft_rows_tw_kernel<L, -1>;
     auto ck = fft_cols_tw_kernel<L, -1>;
     if ((e = cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm)) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm)) != cudaSuccess) return e;
     rk<<<(nrows + gpc - 1) / gpc, gpc * T, rsm, s>>>(in, out, nrows, tw);
-    ck<<<dim3(L / ColGeo<L>::CW, batch), ColGeo<L>::THREADS, csm, s>>>(out, tw);
+    ck<<<dim3(L / ColGeo<L>::CW, batch), ColGeo<L>::THREADS, csm, s>>>(out, tw, col_wave<L>(ck, csm, batch));
   }
   return cudaGetLastError();
 }
