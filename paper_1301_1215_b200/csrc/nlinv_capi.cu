@@ -863,10 +863,6 @@ nlinv_status enq_set_point(Enq& q, const float2* x, float2* fwd_out, bool t_read
   ra.in = pl->tA;
   ra.xrho = x;
   ra.out = fwd_out;
-  if (std::getenv("NLINV_DEBUG_PTRS"))
-    std::fprintf(stderr, "set_point: tA=%p tB=%p x=%p c_omega=%p rho_omega=%p slab=%p J=%d sizeof(RowArgs)=%zu\n",
-                 (void*)pl->tA, (void*)pl->tB, (const void*)x, (void*)pl->c_omega, (void*)pl->rho_omega, pl->slab, pl->J,
-                 sizeof(RowArgs));
   TRY(q.row(fwd_out ? RK_SETPOINT_FWD : RK_SETPOINT, ra));
   return NLINV_OK;
 }
