@@ -305,13 +305,12 @@ def test_reconstruct_c4_newton_step_32_coils():
     plan.close()
 
 
-@pytest.mark.parametrize("J", [1, 2])
-def test_reconstruct_few_local_coils(J):
-    """A coil-sharded rank's load at the C2 grid (1 or 2 local coils, 384^2): the fused pass tops its CTA
+@pytest.mark.parametrize("ng,J", [(384, 1), (384, 2), (512, 1), (192, 1)])
+def test_reconstruct_few_local_coils(ng, J):
+    """A coil-sharded rank's load (1 or 2 local coils at 192^2, 384^2, 512^2): the fused pass tops its CTA
     grid up with rho-only CTAs (k5cg_rows) so the replicated rho block's stripes stay small; 2 Newton x 4 CG
     (the last CG iteration's Newton update included), then a warm second frame, vs the oracle."""
     B = _B()
-    ng = 384
     y, mask = _frame(ng, J, 15, 5)
     plan = B.Plan(ng, J, mask)
     x, img = plan.reconstruct(dev(y), None, 2, 4)
