@@ -357,7 +357,8 @@ VARIANTS = {
 def test_execution_variants_match_oracle(variant, ng, J, spokes, turns, K, L):
     """Every execution path of the library (read from the environment at plan creation) gives
     the oracle's frame: the fused cooperative passes, the unfused multi-kernel path used for
-    world > 1, and the persistent frame kernel (barrier and dataflow schedules)."""
+    world > 1 (NCCL transport, on a one-rank communicator), the cluster-fused K2-K3-K4 pass and the cp.async
+    (no-TMA) tile prefetch."""
     B = _B()
     old = {k: os.environ.get(k) for k in VARIANTS[variant]}
     os.environ.update(VARIANTS[variant])
