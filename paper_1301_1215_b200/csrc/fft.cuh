@@ -391,7 +391,25 @@ struct Sched {
   static constexpr int out_off(int e) { return C::T * (e / RL) + (e % RL) * (L / RL); }
 };
 
-// Twiddle from the shared table tw[m] = e^{-2 pi i m / L}; DIR = +1 conjugates.
+// Inter-pass twiddle table, one block per pass p >= 1 (NS = R0 ... R_{p-1} points already combined, radix
+// R = R_p), laid out [r - 1][k]: entry tw_base(NS) + (r - 1) NS + k = e^{-2 pi i k r / (NS R)}, k < NS,
+// 1 <= r < R. Threads of a row transform hold consecutive k, so a warp's twiddle loads hit consecutive
+// words (conflict-free) instead of the stride k r L / (NS R) of a plain e^{-2 pi i m / L} table (up to
+// 16-way bank conflicts). At most L entries for every schedule here; built on the host (nlinv_plan_create).
+template <int L>
+__host__ __device__ constexpr int tw_base(int NS) {
+  using C = Cfg<L>;
+  const int Rs[4] = {C::R0, C::R1, C::R2, C::R3};
+  int base = 0, ns = C::R0;
+  for (int p = 1; p < C::NP; ++p) {
+    if (ns == NS) return base;
+    base += ns * (Rs[p] - 1);
+    ns *= Rs[p];
+  }
+  return base;
+}
+
+// Twiddle from the shared table (entry m); DIR = +1 conjugates.
 template <int DIR>
 __device__ __forceinline__ float2 twid(const float2* tw, int m) {
   float2 w = tw[m];
@@ -409,7 +427,7 @@ __device__ __forceinline__ void pass_compute(float2* v, int t, const float2* tw)
       const int j = t + T * m;
       const int k = j % NS;
 #pragma unroll
-      for (int r = 1; r < R; ++r) v[m * R + r] = cmul(v[m * R + r], twid<DIR>(tw, k * r * (L / (NS * R))));
+      for (int r = 1; r < R; ++r) v[m * R + r] = cmul(v[m * R + r], twid<DIR>(tw, tw_base<L>(NS) + (r - 1) * NS + k));
     }
     DFT<R, DIR>::run(&v[m * R]);
   }

@@ -661,11 +661,28 @@ extern "C" nlinv_status nlinv_plan_create(int nx, int ny, int ncoils, const uint
     cudaGetLastError();
     return fail(nullptr, NLINV_ERR_NOMEM, "device allocation failed");
   }
-  // one-time tables in fp64, rounded to fp32 (R2): twiddles e^{-2 pi i m / ng}, w^{-1}(k)
-  std::vector<float2> tw(nx);
-  for (int m = 0; m < nx; ++m) {
-    const double ang = 2.0 * M_PI * (double)m / (double)nx;
-    tw[m] = make_float2((float)std::cos(ang), (float)(-std::sin(ang)));
+  // one-time tables in fp64, rounded to fp32 (R2): the inter-pass twiddles e^{-2 pi i m / ng} of every
+  // Stockham pass p >= 1 in the pass's [r - 1][k] block (m = k r ng / (NS R), fft.cuh tw_base), w^{-1}(k)
+  std::vector<float2> tw(nx, make_float2(0.f, 0.f));
+  {
+    int R[4] = {1, 1, 1, 1};
+    const int np = fft_radices(nx, R);
+    size_t off = 0;
+    int NS = R[0];
+    for (int p = 1; p < np; ++p) {
+      for (int r = 1; r < R[p]; ++r)
+        for (int k = 0; k < NS; ++k) {
+          const long long m = (long long)k * r * (nx / (NS * R[p]));
+          const double ang = 2.0 * M_PI * (double)m / (double)nx;
+          tw[off + (size_t)(r - 1) * NS + k] = make_float2((float)std::cos(ang), (float)(-std::sin(ang)));
+        }
+      off += (size_t)NS * (R[p] - 1);
+      NS *= R[p];
+    }
+    if (off > (size_t)nx) {
+      plan_free(pl);
+      return fail(nullptr, NLINV_ERR_SIZE, "twiddle table exceeds ng entries");
+    }
   }
   std::vector<float> wi(N);
   const double a = prm.sob_a, b = prm.sob_b;

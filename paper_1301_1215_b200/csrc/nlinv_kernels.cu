@@ -22,6 +22,13 @@ int row_pairs_override() {
   return v;
 }
 
+int fft_radices(int ng, int* R) {
+#define X(L) if (ng == L) { R[0] = Cfg<L>::R0; R[1] = Cfg<L>::R1; R[2] = Cfg<L>::R2; R[3] = Cfg<L>::R3; return Cfg<L>::NP; }
+  NLV_FOR_EACH_NG(X)
+#undef X
+  return 0;
+}
+
 int k4_planes(int ng, int J) {
 #define X(L) if (ng == L) { const int c = k4_chunk_t<L>(J); return (J + c - 1) / c; }
   NLV_FOR_EACH_NG(X)

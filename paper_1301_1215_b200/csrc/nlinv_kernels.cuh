@@ -138,6 +138,7 @@ struct RowArgs {
   int stage;               // K2: stage c|Omega, rho|Omega, p_rho rows in shared memory (set by the launcher)
 };
 int k4_planes(int ng, int J);  // number of K4 coil-sum planes
+int fft_radices(int ng, int* R);  // radices R[0..NP-1] of the length-ng transform's Stockham passes; returns NP
 
 struct VecArgs {
   float2* x;         // unknowns (CG update of the last iteration adds into x)
