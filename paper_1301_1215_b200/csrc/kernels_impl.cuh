@@ -51,7 +51,12 @@ struct ColBuf {
   float2* s;
   int c;
   __device__ __forceinline__ float2& operator()(int i) const { return s[i * CW + c]; }
+  // (a row swap keyed by t & 1 removes the 2-way conflicts of the pass-0 stores at CW = 8, L >= 512, but
+  // measured no faster: the column passes there are not bound by these stores)
+  template <int L>
   __device__ __forceinline__ float2& first(int i) const { return s[i * CW + c]; }
+  template <int L>
+  __device__ __forceinline__ float2& mid(int i) const { return s[i * CW + c]; }
 };
 // Row exchange buffer. The first Stockham exchange (buf.first) is XOR-swizzled: slot i lives at
 // (i & ~15) | ((i & 15) ^ ((i >> 4) & 15)). The first pass stores at stride R (8 at L = 384, 16 at
@@ -63,7 +68,19 @@ struct RowBuf {
   __device__ __forceinline__ float2& operator()(int i) const { return s[i]; }
   // first Stockham exchange only (the stride-R stores): the later exchanges are conflict-light
   // unswizzled, and the swizzle's index arithmetic is not free in these issue-bound passes
+  template <int L>
   __device__ __forceinline__ float2& first(int i) const { return s[(i & ~15) | ((i & 15) ^ ((i >> 4) & 15))]; }
+  // second exchange (after pass 1, stride NS = R0 stores): unswizzled, the threads t and t + R0 of a
+  // row (and the rows sharing a warp) land on the same 8-byte banks at L = 384 / 512 / 768 (2-way
+  // conflicts); an XOR of the bit that separates them into bank bit 3 (a full 4-bit key at 512) makes
+  // the stores conflict-free and keeps the contiguous reads "t + T m + const" conflict-free
+  template <int L>
+  __device__ __forceinline__ float2& mid(int i) const {
+    if constexpr (L == 384) return s[i ^ (((i >> 4) & 1) << 3)];
+    else if constexpr (L == 512) return s[(i & ~15) | ((i & 15) ^ ((i >> 4) & 15))];
+    else if constexpr (L == 768) return s[i ^ (((i >> 5) & 1) << 3)];
+    else return s[i];
+  }
 };
 
 __device__ __forceinline__ float sgn_of(int i) { return (i & 1) ? -1.0f : 1.0f; }
