@@ -1,0 +1,11 @@
+#!/bin/bash
+# r02d evidence on the final code
+TAG=r02d
+mkdir -p gpurun_out
+bash tools/gpu_round.sh $TAG > gpurun_out/${TAG}_round.txt 2>&1
+bash tools/profile.sh > /dev/null 2>&1
+timeout 600 python tools/bench_stream.py --coils 32 --frames 200 > gpurun_out/${TAG}_c4.log 2>&1
+timeout 600 python tools/bench_stream.py --coils 8 --ng 32 --spokes 8 --turns 1 --newton 3 --frames 200 > gpurun_out/${TAG}_c1.log 2>&1
+timeout 900 python tools/bench_ops.py > gpurun_out/${TAG}_c5.log 2>&1
+bash tools/smallj.sh base > gpurun_out/${TAG}_smallj.txt 2>&1
+cat gpurun_out/${TAG}_round.txt; tail -1 gpurun_out/${TAG}_c4.log | head -c 600; echo; cat gpurun_out/${TAG}_smallj.txt
