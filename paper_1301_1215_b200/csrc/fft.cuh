@@ -447,7 +447,7 @@ __device__ __forceinline__ void pass_exchange(float2* v, int t, BUF& buf, SYNC s
     const int base = (j / NS) * NS * R + (j % NS);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      if constexpr (NS == 1) buf.template first<L>(base + r * NS) = v[m * R + r];
+      if constexpr (NS == 1) buf.template first_st<L>(base + r * NS, r & 1) = v[m * R + r];
       else if constexpr (NS == C::R0) buf.template mid<L>(base + r * NS) = v[m * R + r];
       else buf(base + r * NS) = v[m * R + r];
     }
@@ -457,7 +457,7 @@ __device__ __forceinline__ void pass_exchange(float2* v, int t, BUF& buf, SYNC s
   for (int m = 0; m < E / RN; ++m) {
 #pragma unroll
     for (int r = 0; r < RN; ++r) {
-      if constexpr (NS == 1) v[m * RN + r] = buf.template first<L>(t + T * m + r * (L / RN));
+      if constexpr (NS == 1) v[m * RN + r] = buf.template first_ld<L>(t + T * m + r * (L / RN));
       else if constexpr (NS == C::R0) v[m * RN + r] = buf.template mid<L>(t + T * m + r * (L / RN));
       else v[m * RN + r] = buf(t + T * m + r * (L / RN));
     }

@@ -51,10 +51,34 @@ struct ColBuf {
   float2* s;
   int c;
   __device__ __forceinline__ float2& operator()(int i) const { return s[i * CW + c]; }
-  // (a row swap keyed by t & 1 removes the 2-way conflicts of the pass-0 stores at CW = 8, L >= 512, but
-  // measured no faster: the column passes there are not bound by these stores)
   template <int L>
   __device__ __forceinline__ float2& first(int i) const { return s[i * CW + c]; }
+  // First exchange at CW = 8 (L >= 512): pass 0 stores rows i = (t + T m) R0 + r, so the 4 t-values of
+  // a warp are R0 rows apart and hit the same 8-byte banks (2-way conflicts). Rows i and i ^ 1 are
+  // swapped when bit log2(R0) of i is set: for the stores that bit is t & 1 and the parity of i is r's,
+  // for the loads (i = t + T m + r L / RN) both are bits of t, so the swap is a per-thread row offset
+  // folded into the column offset -- no instruction per access.
+  static constexpr bool kSwz1(int L) { return CW == 8 && (L == 512 || L == 768 || L == 1024); }
+  template <int L>
+  __device__ __forceinline__ float2& first_st(int i, int rpar) const {   // rpar = r & 1 (unrolled: constant)
+    if constexpr (kSwz1(L)) {
+      const int key = (int)(threadIdx.x / CW) & 1;   // t & 1
+      return s[i * CW + c + (rpar ? -key : key) * CW];
+    } else {
+      return s[i * CW + c];
+    }
+  }
+  template <int L>
+  __device__ __forceinline__ float2& first_ld(int i) const {
+    if constexpr (kSwz1(L)) {
+      constexpr int lg = Cfg<L>::R0 == 16 ? 4 : 3;
+      const int t = (int)(threadIdx.x / CW);
+      const int d = ((t >> lg) & 1) ? ((t & 1) ? -1 : 1) : 0;
+      return s[i * CW + c + d * CW];
+    } else {
+      return s[i * CW + c];
+    }
+  }
   template <int L>
   __device__ __forceinline__ float2& mid(int i) const { return s[i * CW + c]; }
 };
@@ -70,6 +94,10 @@ struct RowBuf {
   // unswizzled, and the swizzle's index arithmetic is not free in these issue-bound passes
   template <int L>
   __device__ __forceinline__ float2& first(int i) const { return s[(i & ~15) | ((i & 15) ^ ((i >> 4) & 15))]; }
+  template <int L>
+  __device__ __forceinline__ float2& first_st(int i, int) const { return first<L>(i); }
+  template <int L>
+  __device__ __forceinline__ float2& first_ld(int i) const { return first<L>(i); }
   // second exchange (after pass 1, stride NS = R0 stores): unswizzled, the threads t and t + R0 of a
   // row (and the rows sharing a warp) land on the same 8-byte banks at L = 384 / 512 / 768 (2-way
   // conflicts); an XOR of the bit that separates them into bank bit 3 (a full 4-bit key at 512) makes
