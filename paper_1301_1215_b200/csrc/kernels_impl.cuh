@@ -1562,8 +1562,11 @@ struct RowGeo {
   static constexpr size_t SMEM_K2 = sizeof(float2) * ((size_t)L * (GPC + 1) + (size_t)GPC * 3 * (L / 2));
 };
 
-template <int L, int MODE, bool XP = false>   // XP: K4 with the peer-memory exchange (its own instantiation)
-__global__ void __launch_bounds__(256, NLV_MINB) row_kernel(RowArgs a, const float2* __restrict__ twg) {
+// XP: K4 with the peer-memory exchange (its own instantiation). ONE: register bound for one CTA per SM,
+// used for K2 when its grid is a single wave of one CTA per SM anyway (C2: 144 CTAs on 148 SMs), where the
+// two-CTA bound (128 registers) only makes it spill
+template <int L, int MODE, bool XP = false, bool ONE = false>
+__global__ void __launch_bounds__(256, ONE ? 1 : NLV_MINB) row_kernel(RowArgs a, const float2* __restrict__ twg) {
   extern __shared__ float4 smem_raw[];
   float2* tw = reinterpret_cast<float2*>(smem_raw);
   float2* xb = tw + L;
@@ -1970,9 +1973,10 @@ static cudaError_t launch_row_t(const RowArgs& a0, const float2* tw, cudaStream_
       RowArgs a = a0;
       a.stage = (sm2 <= 115712 || grid <= nsm) ? 1 : 0;
       const size_t shm = a.stage ? (sm2 > smem ? sm2 : smem) : smem;
-      if (shm > smem && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm)) != cudaSuccess)
+      auto k2 = (grid <= nsm && k2_one_enabled()) ? row_kernel<L, MODE, false, true> : kern;
+      if ((e = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(shm > smem ? shm : smem))) != cudaSuccess)
         return e;
-      return launch_k(kern, dim3(grid), dim3(gpc * Cfg<L>::T), shm, s, a, tw);
+      return launch_k(k2, dim3(grid), dim3(gpc * Cfg<L>::T), shm, s, a, tw);
     }
     return launch_k(kern, dim3(grid), dim3(gpc * Cfg<L>::T), smem, s, a0, tw);
   }
@@ -2089,6 +2093,7 @@ static cudaError_t preload_l() {
   get((const void*)row_kernel<L, RK_SETPOINT_FWD>);
   get((const void*)row_kernel<L, RK_RSS>);
   get((const void*)row_kernel<L, RK_K2>);
+  get((const void*)row_kernel<L, RK_K2, false, true>);
   get((const void*)row_kernel<L, RK_K4>);
   if constexpr (K234Geo<L>::kOk) get((const void*)k234_kernel<L>);
   return e;

@@ -36,6 +36,14 @@ int k4_planes(int ng, int J) {
   return J;
 }
 
+bool k2_one_enabled() {   // NLINV_K2ONE=0: K2 always with the two-CTA register bound
+  static const bool on = [] {
+    const char* e = std::getenv("NLINV_K2ONE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("NLINV_PDL");

@@ -170,6 +170,7 @@ cudaError_t launch_fft2d(int ng, const float2* in, float2* out, int batch, int i
                          float2* tmp, cudaStream_t s);
 bool supported_ng(int ng);
 bool pdl_enabled();
+bool k2_one_enabled();
 int col_tiles(int ng);  // column-kernel CTAs per coil
 cudaError_t launch_init_x(float2* x, long long nrho, long long ntot, cudaStream_t s);
 cudaError_t launch_mask_compact(const uint8_t* mask, int N, int* counts, int* idx, int* nnz, cudaStream_t s);
