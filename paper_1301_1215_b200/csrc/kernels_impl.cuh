@@ -811,7 +811,7 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColAr
 // must be the directly computed one: feeding the expanded value back into the next expansion
 // accumulates its absolute error and ruins late iterations (measured in an fp32 model: 5e-2 on
 // the C1 image vs 6e-5 with the direct <r_i,r_i>).
-template <int L, bool XP>
+template <int L, bool XP, bool LAST>
 __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, float2* xb, float2* pf, double* red,
                                           const float* wt) {
   using C = Cfg<L>;
@@ -827,7 +827,10 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   // CTA rows j >= J carry no coil tile, only their stripe of the rho block: with few local coils (a
   // coil-sharded rank) the N-element rho stripe work would otherwise fall on 24 J CTAs (k5cg_rows)
   const bool tcta = j < a.J;
-  const bool last = a.last_iter != 0, hasdx = a.iter > 0;
+  // the last CG iteration (Newton update) and the others are separate instantiations: each launch's
+  // code is one path only (the kernel is large; smaller per-launch code means fewer instruction misses)
+  constexpr bool last = LAST;
+  const bool hasdx = a.iter > 0;
   const unsigned nb = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
   ColBuf<CW> buf{xb, c};
   // w^-1 at k-space row k of this thread's column (global index i): the folded shared table or global memory
@@ -1251,7 +1254,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   }
 }
 
-template <int L, bool XP>
+template <int L, bool XP, bool LAST = false>
 __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) k5cg_kernel(ColArgs a, const float2* __restrict__ twg) {
   constexpr int CW = ColGeo<L>::CW;
   extern __shared__ __align__(128) float4 smem_raw[];   // pf (TMA destination) is 128-byte aligned
@@ -1274,7 +1277,7 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) k5cg_kernel(ColA
     }
   }
   tw_copy_async(tw, twg, L);
-  k5cg_task<L, XP>(a, tw, xb, pf, red, wt);   // griddepcontrol.wait inside, after the r prefetch
+  k5cg_task<L, XP, LAST>(a, tw, xb, pf, red, wt);   // griddepcontrol.wait inside, after the r prefetch
 }
 
 // ------------------------------------------------------------------ row task (one (coil, Omega row) per group)
@@ -1872,7 +1875,9 @@ static bool k5cg_fusable_l(int J) {
   if (ColGeo<L>::THREADS < 64) return false;
   auto kern = k5cg_kernel<L, false>;
   const size_t smem = ColGeo<L>::SMEM_PF;
-  if (cudaFuncSetAttribute(k5cg_kernel<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  if (cudaFuncSetAttribute(k5cg_kernel<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k5cg_kernel<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k5cg_kernel<L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return false;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return false;
   int dev = 0, nsm = 0, per = 0;
@@ -1884,7 +1889,8 @@ static bool k5cg_fusable_l(int J) {
 
 template <int L>
 static cudaError_t launch_k5cg_t(const ColArgs& a, const float2* tw, cudaStream_t s) {
-  auto kern = a.xp != nullptr ? k5cg_kernel<L, true> : k5cg_kernel<L, false>;
+  auto kern = a.xp != nullptr ? (a.last_iter ? k5cg_kernel<L, true, true> : k5cg_kernel<L, true, false>)
+                              : (a.last_iter ? k5cg_kernel<L, false, true> : k5cg_kernel<L, false, false>);
   const size_t smem = ColGeo<L>::SMEM_PF;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -2085,6 +2091,8 @@ static cudaError_t preload_l() {
   get((const void*)col_kernel<L, CK_FFT_W_ADJ, false>);
   get((const void*)k5cg_kernel<L, false>);
   get((const void*)k5cg_kernel<L, true>);
+  get((const void*)k5cg_kernel<L, false, true>);
+  get((const void*)k5cg_kernel<L, true, true>);
   get((const void*)col_kernel<L, CK_FFT_W_NORMAL, false, true>);
   get((const void*)col_kernel<L, CK_FFT_W_RHS, false, true>);
   get((const void*)col_kernel<L, CK_FFT_W_ADJ, false, true>);
