@@ -811,7 +811,7 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColAr
 // must be the directly computed one: feeding the expanded value back into the next expansion
 // accumulates its absolute error and ruins late iterations (measured in an fp32 model: 5e-2 on
 // the C1 image vs 6e-5 with the direct <r_i,r_i>).
-template <int L, bool XP, bool LAST>
+template <int L, bool XP, bool LAST, bool TM>
 __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, float2* xb, float2* pf, double* red,
                                           const float* wt) {
   using C = Cfg<L>;
@@ -858,18 +858,20 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   __shared__ alignas(8) uint64_t pf_bar;
   // p tile by TMA into the exchange buffer once the column FFT no longer needs it (p is parked there)
   __shared__ alignas(8) uint64_t pp_bar;
-  const bool p_tma = a.tmap_p != nullptr && tcta;
+  // TM: the TMA tensor maps exist (default; NLINV_TMA=0 builds the plan without them) -- a template
+  // parameter, so the p-tile branches of the per-element loops fold away
+  const bool p_tma = TM && tcta;
   if (p_tma && tid == 0) tma_bar_init(&pp_bar);   // visible to the CTA at the FFT's first block barrier
   const void* tmap = last ? a.tmap_dx : a.tmap_r;
   if (!tcta) {
     // rho-only CTA: no tile prefetch
-  } else if (tmap != nullptr && (!last || hasdx)) {   // TMA (UTMALDG): one thread issues the tile loads
+  } else if (TM && (!last || hasdx)) {   // TMA (UTMALDG): one thread issues the tile loads
     if (tid == 0) tma_tile_issue(&pf_bar, pf, tmap, tile * CW, j, L, CW);
     pf_tma = true;
-  } else if (!last) {
+  } else if (!TM && !last) {
     tile_prefetch<L, CW>(pf, a.r + j * N, tile * CW);
     pf_on = true;
-  } else if (hasdx) {
+  } else if (!TM && hasdx) {
     tile_prefetch<L, CW>(pf, a.dx + j * N, tile * CW);
     pf_on = true;
   }
@@ -1254,7 +1256,7 @@ __device__ __forceinline__ void k5cg_task(const ColArgs& a, const float2* tw, fl
   }
 }
 
-template <int L, bool XP, bool LAST = false>
+template <int L, bool XP, bool LAST = false, bool TM = true>
 __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) k5cg_kernel(ColArgs a, const float2* __restrict__ twg) {
   constexpr int CW = ColGeo<L>::CW;
   extern __shared__ __align__(128) float4 smem_raw[];   // pf (TMA destination) is 128-byte aligned
@@ -1277,7 +1279,7 @@ __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) k5cg_kernel(ColA
     }
   }
   tw_copy_async(tw, twg, L);
-  k5cg_task<L, XP, LAST>(a, tw, xb, pf, red, wt);   // griddepcontrol.wait inside, after the r prefetch
+  k5cg_task<L, XP, LAST, TM>(a, tw, xb, pf, red, wt);   // griddepcontrol.wait inside, after the r prefetch
 }
 
 // ------------------------------------------------------------------ row task (one (coil, Omega row) per group)
@@ -1877,7 +1879,11 @@ static bool k5cg_fusable_l(int J) {
   const size_t smem = ColGeo<L>::SMEM_PF;
   if (cudaFuncSetAttribute(k5cg_kernel<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
       cudaFuncSetAttribute(k5cg_kernel<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-      cudaFuncSetAttribute(k5cg_kernel<L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      cudaFuncSetAttribute(k5cg_kernel<L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k5cg_kernel<L, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k5cg_kernel<L, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k5cg_kernel<L, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k5cg_kernel<L, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return false;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return false;
   int dev = 0, nsm = 0, per = 0;
@@ -1889,8 +1895,11 @@ static bool k5cg_fusable_l(int J) {
 
 template <int L>
 static cudaError_t launch_k5cg_t(const ColArgs& a, const float2* tw, cudaStream_t s) {
-  auto kern = a.xp != nullptr ? (a.last_iter ? k5cg_kernel<L, true, true> : k5cg_kernel<L, true, false>)
-                              : (a.last_iter ? k5cg_kernel<L, false, true> : k5cg_kernel<L, false, false>);
+  auto kern = a.tmap_p != nullptr
+                  ? (a.xp != nullptr ? (a.last_iter ? k5cg_kernel<L, true, true> : k5cg_kernel<L, true, false>)
+                                     : (a.last_iter ? k5cg_kernel<L, false, true> : k5cg_kernel<L, false, false>))
+                  : (a.xp != nullptr ? (a.last_iter ? k5cg_kernel<L, true, true, false> : k5cg_kernel<L, true, false, false>)
+                                     : (a.last_iter ? k5cg_kernel<L, false, true, false> : k5cg_kernel<L, false, false, false>));
   const size_t smem = ColGeo<L>::SMEM_PF;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -2093,6 +2102,10 @@ static cudaError_t preload_l() {
   get((const void*)k5cg_kernel<L, true>);
   get((const void*)k5cg_kernel<L, false, true>);
   get((const void*)k5cg_kernel<L, true, true>);
+  get((const void*)k5cg_kernel<L, false, false, false>);
+  get((const void*)k5cg_kernel<L, true, false, false>);
+  get((const void*)k5cg_kernel<L, false, true, false>);
+  get((const void*)k5cg_kernel<L, true, true, false>);
   get((const void*)col_kernel<L, CK_FFT_W_NORMAL, false, true>);
   get((const void*)col_kernel<L, CK_FFT_W_RHS, false, true>);
   get((const void*)col_kernel<L, CK_FFT_W_ADJ, false, true>);
