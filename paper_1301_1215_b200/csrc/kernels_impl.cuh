@@ -1593,7 +1593,7 @@ __global__ void __launch_bounds__(256, ONE ? 1 : NLV_MINB) row_kernel(RowArgs a,
   } else if constexpr (MODE == RK_K2) {
     // per-group staging of c_j|Omega, rho|Omega, p_rho|Omega after the exchange buffers (RowGeo::SMEM_K2)
     const int gpc = blockDim.x / Cfg<L>::T;
-    if (a.stage) {
+    if (ONE || a.stage) {   // the one-CTA-per-SM instantiation is launched only with staging on
       row_task<L, MODE>(a, blockIdx.x * gpc, tw, xb, true, xb + (size_t)L * gpc);
     } else {
       pdl_wait();
