@@ -738,11 +738,14 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
   }
 }
 
-template <int L, int MODE, bool PW = false, bool XP = false>   // PW, XP: see col_task
 #ifndef NLV_MINB
 #define NLV_MINB 2  // <= 128 registers: two 256-thread CTAs per SM (more registers halve residency)
 #endif
+// PW, XP: see col_task. CG1: the single-reduction CG flag (K1 and K5 of the unfused CG) as a compile-time
+// constant, so each instantiation holds only the code its launches run
+template <int L, int MODE, bool PW = false, bool XP = false, bool CG1 = false>
 __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColArgs a, const float2* __restrict__ twg) {
+  a.cg1 = CG1 ? 1 : 0;
   constexpr int CW = ColGeo<L>::CW;
   extern __shared__ float4 smem_raw[];
   float2* tw = reinterpret_cast<float2*>(smem_raw);
@@ -1570,7 +1573,9 @@ struct RowGeo {
 // XP: K4 with the peer-memory exchange (its own instantiation). ONE: register bound for one CTA per SM,
 // used for K2 when its grid is a single wave of one CTA per SM anyway (C2: 144 CTAs on 148 SMs), where the
 // two-CTA bound (128 registers) only makes it spill
-template <int L, int MODE, bool XP = false, bool ONE = false>
+// UNST: K2 without the shared-memory staging (grids above one wave whose staging would cost residency);
+// the default instantiation of K2 is compiled for the staged path only
+template <int L, int MODE, bool XP = false, bool ONE = false, bool UNST = false>
 __global__ void __launch_bounds__(256, ONE ? 1 : NLV_MINB) row_kernel(RowArgs a, const float2* __restrict__ twg) {
   extern __shared__ float4 smem_raw[];
   float2* tw = reinterpret_cast<float2*>(smem_raw);
@@ -1593,7 +1598,7 @@ __global__ void __launch_bounds__(256, ONE ? 1 : NLV_MINB) row_kernel(RowArgs a,
   } else if constexpr (MODE == RK_K2) {
     // per-group staging of c_j|Omega, rho|Omega, p_rho|Omega after the exchange buffers (RowGeo::SMEM_K2)
     const int gpc = blockDim.x / Cfg<L>::T;
-    if (ONE || a.stage) {   // the one-CTA-per-SM instantiation is launched only with staging on
+    if constexpr (!UNST) {   // the launcher picks the instantiation from its staging decision
       row_task<L, MODE>(a, blockIdx.x * gpc, tw, xb, true, xb + (size_t)L * gpc);
     } else {
       pdl_wait();
@@ -1932,9 +1937,13 @@ template <int L, int MODE>
 static cudaError_t launch_col_t(const ColArgs& a, const float2* tw, cudaStream_t s) {
   constexpr bool kPWable = (MODE == CK_PSF || MODE == CK_RESADJ || MODE == CK_FWDP || MODE == CK_ADJ1);
   constexpr bool kXPable = (MODE == CK_FFT_W_NORMAL || MODE == CK_FFT_W_RHS || MODE == CK_FFT_W_ADJ);
+  constexpr bool kCG = (MODE == CK_IFFT_W_CG || MODE == CK_FFT_W_NORMAL);
   auto kern = (kPWable && a.pw != nullptr) ? col_kernel<L, MODE, kPWable>
               : (kXPable && a.xp != nullptr) ? col_kernel<L, MODE, false, kXPable>
                                            : col_kernel<L, MODE, false>;
+  if constexpr (kCG) {
+    if (a.cg1) kern = (kXPable && a.xp != nullptr) ? col_kernel<L, MODE, false, kXPable, true> : col_kernel<L, MODE, false, false, true>;
+  }
   const size_t smem = ColGeo<L>::SMEM;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -1988,7 +1997,8 @@ static cudaError_t launch_row_t(const RowArgs& a0, const float2* tw, cudaStream_
       RowArgs a = a0;
       a.stage = (sm2 <= 115712 || grid <= nsm) ? 1 : 0;
       const size_t shm = a.stage ? (sm2 > smem ? sm2 : smem) : smem;
-      auto k2 = (grid <= nsm && k2_one_enabled()) ? row_kernel<L, MODE, false, true> : kern;
+      auto k2 = !a.stage ? row_kernel<L, MODE, false, false, true>
+                : (grid <= nsm && k2_one_enabled()) ? row_kernel<L, MODE, false, true> : kern;
       if ((e = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(shm > smem ? shm : smem))) != cudaSuccess)
         return e;
       return launch_k(k2, dim3(grid), dim3(gpc * Cfg<L>::T), shm, s, a, tw);
@@ -2109,12 +2119,16 @@ static cudaError_t preload_l() {
   get((const void*)col_kernel<L, CK_FFT_W_NORMAL, false, true>);
   get((const void*)col_kernel<L, CK_FFT_W_RHS, false, true>);
   get((const void*)col_kernel<L, CK_FFT_W_ADJ, false, true>);
+  get((const void*)col_kernel<L, CK_IFFT_W_CG, false, false, true>);
+  get((const void*)col_kernel<L, CK_FFT_W_NORMAL, false, false, true>);
+  get((const void*)col_kernel<L, CK_FFT_W_NORMAL, false, true, true>);
   get((const void*)row_kernel<L, RK_K4, true>);
   get((const void*)row_kernel<L, RK_SETPOINT>);
   get((const void*)row_kernel<L, RK_SETPOINT_FWD>);
   get((const void*)row_kernel<L, RK_RSS>);
   get((const void*)row_kernel<L, RK_K2>);
   get((const void*)row_kernel<L, RK_K2, false, true>);
+  get((const void*)row_kernel<L, RK_K2, false, false, true>);
   get((const void*)row_kernel<L, RK_K4>);
   if constexpr (K234Geo<L>::kOk) get((const void*)k234_kernel<L>);
   return e;
