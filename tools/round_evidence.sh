@@ -1,6 +1,6 @@
 #!/bin/bash
 # r02d evidence on the final code
-TAG=r02d
+TAG=${1:-r02e}
 mkdir -p gpurun_out
 bash tools/gpu_round.sh $TAG > gpurun_out/${TAG}_round.txt 2>&1
 bash tools/profile.sh > /dev/null 2>&1
