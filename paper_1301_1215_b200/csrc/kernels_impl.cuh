@@ -743,9 +743,10 @@ __device__ __forceinline__ void col_task(const ColArgs& a, int tile, int j, cons
 #endif
 // PW, XP: see col_task. CG1: the single-reduction CG flag (K1 and K5 of the unfused CG) as a compile-time
 // constant, so each instantiation holds only the code its launches run
-template <int L, int MODE, bool PW = false, bool XP = false, bool CG1 = false>
+template <int L, int MODE, bool PW = false, bool XP = false, bool CG1 = false, bool FK1 = false>
 __global__ void __launch_bounds__(ColGeo<L>::THREADS, NLV_MINB) col_kernel(ColArgs a, const float2* __restrict__ twg) {
   a.cg1 = CG1 ? 1 : 0;
+  if constexpr (MODE == CK_FFT_W_RHS) a.fuse_k1 = FK1 ? 1 : 0;   // the Newton rhs fused with K1 (FK1)
   constexpr int CW = ColGeo<L>::CW;
   extern __shared__ float4 smem_raw[];
   float2* tw = reinterpret_cast<float2*>(smem_raw);
@@ -1944,6 +1945,9 @@ static cudaError_t launch_col_t(const ColArgs& a, const float2* tw, cudaStream_t
   if constexpr (kCG) {
     if (a.cg1) kern = (kXPable && a.xp != nullptr) ? col_kernel<L, MODE, false, kXPable, true> : col_kernel<L, MODE, false, false, true>;
   }
+  if constexpr (MODE == CK_FFT_W_RHS) {
+    if (a.fuse_k1) kern = a.xp != nullptr ? col_kernel<L, MODE, false, true, false, true> : col_kernel<L, MODE, false, false, false, true>;
+  }
   const size_t smem = ColGeo<L>::SMEM;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -2122,6 +2126,8 @@ static cudaError_t preload_l() {
   get((const void*)col_kernel<L, CK_IFFT_W_CG, false, false, true>);
   get((const void*)col_kernel<L, CK_FFT_W_NORMAL, false, false, true>);
   get((const void*)col_kernel<L, CK_FFT_W_NORMAL, false, true, true>);
+  get((const void*)col_kernel<L, CK_FFT_W_RHS, false, false, false, true>);
+  get((const void*)col_kernel<L, CK_FFT_W_RHS, false, true, false, true>);
   get((const void*)row_kernel<L, RK_K4, true>);
   get((const void*)row_kernel<L, RK_SETPOINT>);
   get((const void*)row_kernel<L, RK_SETPOINT_FWD>);

@@ -1,5 +1,5 @@
 #!/bin/bash
-# r02d evidence on the final code
+# round evidence on the final code (TAG = $1): GPU tests, bench, sanitizers, ncu launch lists, C4 / C1 streams, C5 sweep, small-J
 TAG=${1:-r02e}
 mkdir -p gpurun_out
 bash tools/gpu_round.sh $TAG > gpurun_out/${TAG}_round.txt 2>&1
